@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Benchmark of the gDist hot path on B200 (BASELINE.json metric).
+
+Workload (config 2 / 3 of BASELINE.json): two interlocked rings of
+2500 x 1500 quads = 7,500,000 triangles each.  One step on rank r is one
+frame f of the 1000-frame rotation sequence (scenes.ring_frame_transforms):
+refit(A_f), refit(B_f), exact min-distance query.  Frames are sharded
+f = step * N + rank, so per-GPU work is fixed as N grows (weak scaling, no
+collective in the loop).  `value` = whole-job milliseconds per min-distance
+query (refits included): max-over-ranks device time of the K steps / (K N).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the CPU oracle port of the reference algorithm
+(oracle/meshdist_oracle.py; the reference itself is pure Python and does not
+travel to the GPU box) on the same frames, all host threads, bounded steps.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "ms per min/max distance query, 2×7.5M-tri rings; frames/s at 1/2/4/8 GPUs"
+PAPER_MS = 0.38  # rings min query, 2 x 7.5M, RTX 4090
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--nu", type=int, default=2500)
+    ap.add_argument("--nv", type=int, default=1500)
+    ap.add_argument("--kind", choices=["min", "max"], default="min")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=150.0, help="seconds for CPU legs")
+    ap.add_argument("--profile-only", action="store_true", help="a short run for ncu (no baselines)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def query_bytes(res, depth_a, depth_b):
+    """Algorithmic bytes of one query: per iteration
+    front_in*12 + front_in*(2^ka + 2^kb)*24 + front_out*12; narrow phase
+    leaf_pairs*(12 + 2*8) + narrow_pairs*72."""
+    da = db = 0
+    total = 0
+    expand = 0
+    leaf_pairs = 0
+    for s in res.iterations:
+        ka, kb = min(s.k, depth_a - da), min(s.k, depth_b - db)
+        b = s.front_in * 12 + s.front_in * ((1 << ka) + (1 << kb)) * 24 + s.front_out * 12
+        expand += b
+        if s.front_out == 0 and s.k == max(depth_a - da, depth_b - db):
+            leaf_pairs = (s.front_in << (ka + kb)) - s.culled
+        da += ka
+        db += kb
+    narrow = leaf_pairs * (12 + 16) + res.narrow_pairs * 72
+    total = expand + narrow
+    return {"expand_bytes": expand, "narrow_bytes": narrow, "total_bytes": total, "leaf_pairs": leaf_pairs,
+            "narrow_flops": res.narrow_pairs * (2100 if res.kind == "min" else 72)}
+
+
+def peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2411_11244_b200 as md
+    from paper_2411_11244_b200 import _lib
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    t0 = time.time()
+    tz, tb = md.ring_pair_base(args.nu, args.nv)
+    bvh_a, bvh_b = md.build_f12(tz), md.build_f12(tb)
+    setup_s = time.time() - t0
+    cfg = md.EngineConfig(front_hard_cap=1 << 27)
+    K, W, N = args.steps, args.warmup, world
+
+    def frame_meshes(f):
+        xa, xb = md.ring_frame_transforms(f % 1000)
+        return md.apply_transform(tz, xa), md.apply_transform(tb, xb)
+
+    # prepared queries per frame (device views resolved outside the timing)
+    frames = [(s * N + rank) for s in range(W + K)]
+    prepared = []
+    for f in frames:
+        a, b = frame_meshes(f)
+        md.refit(bvh_a, a)
+        md.refit(bvh_b, b)
+        prepared.append((a, b, md.PreparedQuery(a, b, bvh_a, bvh_b, cfg, args.kind)))
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(W + K)]
+
+    def step(i):
+        a, b, pq = prepared[i]
+        e0, e1, e2 = ev[i]
+        e0.record(stream)
+        bvh_a._device_refit(a)
+        bvh_b._device_refit(b)
+        e1.record(stream)
+        pq.launch()
+        e2.record(stream)
+
+    for i in range(W):
+        step(i)
+        prepared[i][2].collect()
+    torch.cuda.synchronize()
+    launches0 = _lib.lib().gd_launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for i in range(W, W + K):
+            step(i)
+        end.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.lib().gd_launch_count() - launches0
+    if dist:
+        dist.barrier()
+    region_ms = start.elapsed_time(end)
+    refit_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(W, W + K)]
+    query_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(W, W + K)]
+    # results of every timed query (read after the region)
+    results = []
+    for i in range(W, W + K):
+        a, b, pq = prepared[i]
+        pq.launch()  # re-run to read back stats (the timed launches share one workspace)
+        results.append(pq.collect())
+    if dist:
+        t = torch.tensor([region_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        region_ms = float(t.item())
+
+    # phase breakdown + roofline on one extra (untimed) query of the last frame
+    L = _lib.lib()
+    L.gd_set_profiling(1)
+    a, b, pq = prepared[-1]
+    bvh_a._device_refit(a)
+    bvh_b._device_refit(b)
+    pq.launch()
+    res = pq.collect()
+    import ctypes as C
+
+    ph = (C.c_float * 5)()
+    L.gd_query_phase_ms(ph, 5)
+    L.gd_set_profiling(0)
+    phases = {"init": ph[0], "expand": ph[1], "narrow": ph[2], "exact": ph[3], "final": ph[4]}
+    qb = query_bytes(res, bvh_a.depth, bvh_b.depth)
+    hbm, sm_max, src = peaks()
+    expand_ms = phases["expand"]
+    achieved = qb["expand_bytes"] / (expand_ms * 1e-3) / 1e9 if expand_ms > 0 else None
+    roofline = {"bound": "hbm", "kernel": "k_expand (all iterations of one query)", "achieved": achieved,
+                "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None, "traffic": None,
+                "peak_source": src, "algorithmic_bytes": qb["expand_bytes"], "kernel_ms": expand_ms}
+    narrow_tflops = qb["narrow_flops"] / (phases["narrow"] * 1e-3) / 1e12 if phases["narrow"] > 0 else None
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+
+    # e2e through the public API: per step, the frame transforms go host ->
+    # device (kernel parameters) and the result comes back (one D2H)
+    e2e_ms = []
+    torch.cuda.synchronize()
+    for i in range(W, W + K):
+        f = frames[i]
+        t1 = time.perf_counter()
+        xa, xb = md.ring_frame_transforms(f % 1000)
+        a, b = md.apply_transform(tz, xa), md.apply_transform(tb, xb)
+        md.refit(bvh_a, a)
+        md.refit(bvh_b, b)
+        r = (md.run_min_query if args.kind == "min" else md.run_max_query)(a, b, bvh_a, bvh_b, cfg)
+        e2e_ms.append((time.perf_counter() - t1) * 1e3)
+        assert r.distance == results[i - W].distance
+    e2e_step_ms = float(np.mean(e2e_ms))
+    if dist:
+        t = torch.tensor([e2e_step_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step_ms = float(t.item())
+
+    value = region_ms / (K * N)
+    clocks = clk.summary()
+    out = None
+    if rank == 0:
+        out = {
+            "metric": METRIC,
+            "value": round(value, 6),
+            "unit": "ms/query",
+            "n_gpus": N,
+            "steps": K,
+            "warmup": W,
+            "ms_per_step": round(region_ms / K, 6),
+            "higher_is_better": False,
+            "scaling": "weak",
+            "vs_baseline": round(value / PAPER_MS, 4),
+            "dtype": "f32 traversal + f64 exact pass",
+            "data": "synthetic (interlocked tori, rotation sequence frames)",
+            "config": {"workload": f"rings {2 * args.nu * args.nv} tris/mesh (config 2), frame f = step*N + rank; "
+                                   f"step = refit A + refit B + {args.kind} query",
+                       "nu": args.nu, "nv": args.nv, "kind": args.kind, "precision": 64,
+                       "l2": "inputs larger than L2 (2 x 200 MB node boxes rewritten by each step's refits)"},
+            "query_ms": round(float(np.mean(query_ms)), 6),
+            "query_ms_min": round(float(np.min(query_ms)), 6),
+            "refit_ms": round(float(np.mean(refit_ms)), 6),
+            "frames_per_s": round(1000.0 / value, 3),
+            "phases_ms": {k: round(v, 6) for k, v in phases.items()},
+            "distance": results[-1].distance,
+            "witness": [results[-1].witness.tri_a, results[-1].witness.tri_b],
+            "iterations": len(res.iterations),
+            "expanded_pairs": res.expanded_pairs,
+            "narrow_pairs": res.narrow_pairs,
+            "band_pairs": res.band_pairs,
+            "peak_front": res.peak_front,
+            "roofline": roofline,
+            "narrow_fp32": {"achieved_tflops": narrow_tflops, "peak_tflops_nominal": fp32_peak,
+                            "frac": (narrow_tflops / fp32_peak) if narrow_tflops else None},
+            "e2e": {"value": round(e2e_step_ms / N, 6), "unit": "ms/query", "h2d_bytes_per_step": 2 * 96,
+                    "d2h_bytes_per_step": C.sizeof(_lib.GdResult) + 64 * C.sizeof(_lib.GdIterStat),
+                    "note": "public API per frame: apply_transform + refit x2 + run_min_query (sync)"},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "setup_s": round(setup_s, 2),
+        }
+    if dist:
+        dist.barrier()
+    return out, (tz, tb, bvh_a, bvh_b, frames[W:], results)
+
+
+# ---------------------------------------------------------------------------
+def oracle_trees(md, bvh_a, bvh_b):
+    """Oracle trees sharing the device tree's topology (the reference's
+    O(n^2) greedy cannot build 7.5M triangles; pairing parity is tested)."""
+    from oracle import meshdist_oracle as oracle
+
+    ta = oracle.Tree(np.empty((bvh_a.n_nodes, 3)), np.empty((bvh_a.n_nodes, 3)), np.asarray(bvh_a.leaf_tris),
+                     np.asarray(bvh_a.prim_order), bvh_a.depth)
+    tb = oracle.Tree(np.empty((bvh_b.n_nodes, 3)), np.empty((bvh_b.n_nodes, 3)), np.asarray(bvh_b.leaf_tris),
+                     np.asarray(bvh_b.prim_order), bvh_b.depth)
+    return oracle, ta, tb
+
+
+def cpu_frame_query(oracle, ta, tb, tz, tbm, f, kind, workers):
+    """One step of the reference algorithm on the CPU: oracle refit of both
+    meshes for frame f (fill_boxes) + oracle query."""
+    import paper_2411_11244_b200 as md
+
+    xa, xb = md.ring_frame_transforms(f % 1000)
+    va = oracle.transform_vertices(tz.vertices, xa.rotation, xa.translation)
+    vb = oracle.transform_vertices(tbm.vertices, xb.rotation, xb.translation)
+    oracle.fill_boxes(ta, va, tz.triangles)
+    oracle.fill_boxes(tb, vb, tbm.triangles)
+    pa = oracle.triangle_points(va, tz.triangles)
+    pb = oracle.triangle_points(vb, tbm.triangles)
+    return oracle.run_query(ta, tb, pa, pb, kind, oracle.Config(workers=workers))
+
+
+def cpu_baseline(args, ctx, budget):
+    import paper_2411_11244_b200 as md
+
+    tz, tbm, bvh_a, bvh_b, frames, results = ctx
+    oracle, ta, tb = oracle_trees(md, bvh_a, bvh_b)
+    workers = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    r = cpu_frame_query(oracle, ta, tb, tz, tbm, frames[-1], args.kind, workers)
+    sec = time.perf_counter() - t0
+    agree = r.distance == results[-1].distance
+    return {"value": round(sec * 1e3, 3), "unit": "ms/query", "cores": workers, "kind": "port",
+            "sample": f"1 frame (f={frames[-1]}) of the same workload: oracle refit A+B + {args.kind} query, "
+                      f"numpy, {workers} threads",
+            "distance_equal_to_gpu": bool(agree)}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return None
+    import torch
+
+    import paper_2411_11244_b200 as md
+
+    torch.cuda.set_device(local) if torch.cuda.is_available() else None
+    tz, tbm = md.ring_pair_base(args.nu, args.nv)
+    # the tree topology comes from our exact-pairing build (parity-tested
+    # against the reference greedy; the literal O(n^2) greedy does not finish)
+    bvh_a, bvh_b = md.build_f12(tz), md.build_f12(tbm)
+    oracle, ta, tb = oracle_trees(md, bvh_a, bvh_b)
+    workers = os.cpu_count() or 1
+    N = args.gpus
+    W = min(args.warmup, 1)
+    times = []
+    t_start = time.perf_counter()
+    s = 0
+    while s < W + args.steps:
+        f = s * N
+        t0 = time.perf_counter()
+        cpu_frame_query(oracle, ta, tb, tz, tbm, f, args.kind, workers)
+        dt = time.perf_counter() - t0
+        if s >= W:
+            times.append(dt)
+        s += 1
+        if time.perf_counter() - t_start > args.cpu_budget and times:
+            break
+    value = float(np.mean(times)) * 1e3
+    return {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": "ms/query",
+        "n_gpus": N,
+        "steps": len(times),
+        "warmup": W,
+        "ms_per_step": round(value, 3),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (interlocked tori, rotation sequence frames)",
+        "config": {"workload": f"rings {2 * args.nu * args.nv} tris/mesh (config 2), frame f = step*N; step = "
+                               f"refit A + refit B + {args.kind} query", "nu": args.nu, "nv": args.nv,
+                   "kind": args.kind, "precision": 64},
+        "cpu_baseline": {"value": round(value, 3), "unit": "ms/query", "cores": workers, "kind": "port",
+                         "sample": f"{len(times)} frame steps (bounded to {args.cpu_budget:.0f} s) of the same "
+                                   f"workload, oracle port of the reference (numpy, {workers} threads)"},
+        "e2e": {"value": round(value, 3), "unit": "ms/query", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        out = run_reference(args)
+        if out is not None:
+            print(json.dumps(out))
+        return
+    out, ctx = run_ours(args)
+    world, rank, _ = dist_env()
+    if rank == 0 and out is not None:
+        if not args.no_cpu_baseline and not args.profile_only and world == 1:
+            try:
+                out["cpu_baseline"] = cpu_baseline(args, ctx, args.cpu_budget)
+            except Exception as exc:  # report, never hide
+                out["cpu_baseline"] = {"value": None, "error": repr(exc)}
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

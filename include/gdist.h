@@ -1,0 +1,209 @@
+/*
+ * gdist.h -- C ABI of libgdist.so, the B200 (sm_100a) implementation of the
+ * gDist hot path (arXiv 2411.11244): f12-BVH build / refit, BVTT front
+ * traversal with AABB bounds, exact triangle-triangle narrow phase.
+ *
+ * Plain C: no torch / CUDA types in the signatures.  Device memory is owned
+ * by the caller (the Python package allocates it as torch tensors); every
+ * pointer documented "device" must point to CUDA device memory of the current
+ * device, every "host" pointer to host memory.  `stream` is a cudaStream_t
+ * passed as void* (NULL = legacy default stream).
+ *
+ * Every entry point returns a GdStatus; on failure a human-readable message is
+ * available from gd_last_error() (thread-local).  No C++ exception crosses the
+ * boundary.  The reference interface each entry point replaces is cited as
+ * file:line under /root/reference/pkg/src/meshdist/.
+ */
+#ifndef GDIST_H
+#define GDIST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GDIST_ABI_VERSION 1
+
+/* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
+typedef enum GdStatus {
+  GD_OK = 0,
+  GD_ERR_INVALID = 1,        /* ValueError: bad shapes / arguments            */
+  GD_ERR_CONFIG = 2,         /* ConfigError (query.py:77-92, 471-477)          */
+  GD_ERR_TOPOLOGY = 3,       /* TopologyMismatchError (bvh.py:300-304)         */
+  GD_ERR_FRONT_OVERFLOW = 4, /* FrontOverflowError (query.py:373-376, 448-449) */
+  GD_ERR_WORKSPACE = 5,      /* caller workspace too small                     */
+  GD_ERR_CUDA = 6,           /* CUDA runtime failure                           */
+  GD_ERR_NO_DEVICE = 7       /* no CUDA device visible                         */
+} GdStatus;
+
+/* One mesh as seen by the device (mesh.py:21-66 TriangleMesh).  Vertices are
+ * the float64 "base" positions; when has_xf != 0 every vertex is mapped to
+ * R*v + t on the fly (mesh.py:102-105 apply_transform, row-major R). */
+typedef struct GdMesh {
+  const double* vtx;   /* device, (nv, 3) float64                        */
+  const int32_t* tri;  /* device, (m, 3) vertex indices                  */
+  int64_t nv;
+  int64_t m;
+  double rot[9];
+  double trans[3];
+  int32_t has_xf;
+  int32_t _pad;
+} GdMesh;
+
+/* Sizes of an f12-BVH over m triangles (bvh.py:98-111, 184-211). */
+typedef struct GdBvhSizes {
+  int64_t leaf_count; /* L = largest power of two <= m */
+  int64_t n_nodes;    /* 2L - 1                        */
+  int32_t depth;      /* log2(L)                       */
+  int32_t _pad;
+  size_t build_workspace_bytes; /* scratch needed by gd_bvh_build */
+} GdBvhSizes;
+
+/* Device-resident f12-BVH (bvh.py:184-239).  Storage is implicit BFS: node
+ * i has children 2i+1, 2i+2; leaves are the last L nodes.  All arrays are
+ * caller-allocated device memory:
+ *   box        : n_nodes * 6 float32  (minx,miny,minz,maxx,maxy,maxz) per node,
+ *                traversal boxes of the float32-rounded vertices
+ *   leaf_tri   : m * 4 int32  {v0, v1, v2, triangle id} in leaf (Morton) order
+ *   leaf_first : (L + 1) uint32, first leaf_tri slot of each leaf
+ *   vtx32      : nv * 4 float32, transformed float32 vertices (refit output)  */
+typedef struct GdBvh {
+  float* box;
+  int32_t* leaf_tri;
+  uint32_t* leaf_first;
+  float* vtx32;
+  int64_t leaf_count;
+  int64_t n_tris;
+  int64_t nv;
+  int32_t depth;
+  int32_t _pad;
+} GdBvh;
+
+/* EngineConfig (query.py:51-102).  `threads` and `batch_size` have no device
+ * meaning and are not carried. */
+typedef struct GdConfig {
+  int32_t kind;              /* 0 = min query, 1 = max query               */
+  int32_t precision;         /* 32 or 64: arithmetic of the exact pass      */
+  int64_t front_cap;         /* C of the adaptive depth rule               */
+  int32_t depth_cap;
+  int32_t enhanced_bounds;
+  int32_t culling;
+  int32_t guarantee_witness; /* accepted; the engine always keeps ties      */
+  int64_t front_hard_cap;
+  int64_t warm_a;            /* warm_pair triangle ids, -1 = none          */
+  int64_t warm_b;
+  int64_t band_cap;          /* exact-pass candidate buffer entries, 0 = default */
+} GdConfig;
+
+/* QueryResult (query.py:230-263) + Witness (query.py:136-144). */
+typedef struct GdResult {
+  double distance;
+  double witness_distance;
+  double point_a[3];
+  double point_b[3];
+  int64_t tri_a;             /* -1 when no witness                           */
+  int64_t tri_b;
+  int64_t expanded_pairs;
+  int64_t narrow_pairs;
+  int64_t band_pairs;        /* candidates re-evaluated in the exact pass    */
+  int64_t overflow_candidates;
+  int64_t overflow_front_in;
+  int64_t overflow_cap;
+  int32_t iterations;
+  int32_t status;
+} GdResult;
+
+/* IterationStat (query.py:147-162). */
+typedef struct GdIterStat {
+  int64_t front_in;
+  int64_t front_out;
+  int64_t culled;
+  double bound_after;
+  int32_t k;
+  int32_t _pad;
+} GdIterStat;
+
+/* ---- library ---------------------------------------------------------- */
+const char* gd_version(void);
+const char* gd_last_error(void);
+int gd_abi_version(void);
+int gd_device_count(int* count);
+/* number of hot-path kernels (refit + query) launched by this process */
+long long gd_launch_count(void);
+/* phase timing of subsequent queries (CUDA events); gd_query_phase_ms
+ * returns the count written: [init, expand, narrow, exact pass, final] ms */
+int gd_set_profiling(int enable);
+int gd_query_phase_ms(float* out, int n);
+
+/* ---- f12-BVH build / refit (bvh.py) ----------------------------------- */
+/* bvh.py:98-111: L, depth, node count; workspace for gd_bvh_build. */
+int gd_bvh_sizes(int64_t m, int64_t nv, GdBvhSizes* out);
+
+/* build_f12 (bvh.py:267-289): Morton codes (bvh.py:69-95) + radix sort on
+ * the device, exact greedy power-of-two pairing (bvh.py:98-181) on the host,
+ * leaf layout, then a refit.  Writes prim_order (m) and leaf_tris (L, 2)
+ * int64 host arrays with the reference's semantics. */
+int gd_bvh_build(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspace_bytes,
+                 int64_t* prim_order_host, int64_t* leaf_tris_host, void* stream);
+
+/* refit (bvh.py:292-306) with apply_transform (mesh.py:102-105) fused:
+ * transform + f32 vertices, leaf boxes, bottom-up unions. Asynchronous. */
+int gd_refit(const GdMesh* mesh, GdBvh* bvh, void* stream);
+
+/* Node boxes with the reference's dtype semantics (bvh.py:242-264):
+ * precision 64 -> double (n_nodes, 3) min / max, precision 32 -> float.
+ * node_min / node_max are device pointers.  Synchronous. */
+int gd_export_boxes(const GdMesh* mesh, const GdBvh* bvh, int precision, void* node_min,
+                    void* node_max, void* stream);
+
+/* Exact greedy pairing on the host (bvh.py:98-181), exposed for testing:
+ * sa = pair surface areas (n - 1), writes is_left (n bytes, 1 where pair
+ * (i, i+1) merges).  Needs no GPU. */
+int gd_pair_greedy(const double* sa_host, int64_t n, uint8_t* is_left_host);
+
+/* ---- traversal engine (query.py) -------------------------------------- */
+int gd_query_workspace_size(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, size_t* bytes);
+
+/* run_min_query / run_max_query (query.py:480-568).  Synchronous: one
+ * device->host copy of the result at the end.  stats may be NULL. */
+int gd_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+             const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* out,
+             GdIterStat* stats, int max_stats, void* stream);
+
+/* Asynchronous variant: enqueue only; the result is written by the device
+ * into `result_dev` (a device GdResult) -- collect with gd_query_collect. */
+int gd_query_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                   const GdConfig* cfg, void* workspace, size_t workspace_bytes,
+                   GdResult* result_dev, void* stream);
+int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* workspace,
+                     const GdResult* result_dev, GdResult* out, GdIterStat* stats, int max_stats,
+                     void* stream);
+
+/* ---- batch math (bounds.py) ------------------------------------------- */
+/* batch_tri_tri_min / batch_tri_tri_max (bounds.py:245-330), exact
+ * reference arithmetic in `precision` (32 / 64).  t1, t2: device (n, 3, 3);
+ * d: (n); p, q: (n, 3); element type double for 64, float for 32. */
+int gd_tri_tri_batch(int kind, int precision, const void* t1, const void* t2, int64_t n, void* d,
+                     void* p, void* q, void* stream);
+
+/* Fast float32 narrow phase used by the traversal (FMA-contracted): d only.
+ * t1, t2 float (n, 3, 3), d float (n).  For error-bound tests. */
+int gd_tri_tri_fast(int kind, const float* t1, const float* t2, int64_t n, float* d, void* stream);
+
+/* batch_min_lower / batch_max_upper / batch_enhanced_min_upper /
+ * batch_enhanced_max_lower (bounds.py:47-101): which = 0..3.
+ * amin .. bmax: device (n, 3) in `precision`; out (n). */
+int gd_box_bounds_batch(int which, int precision, const void* amin, const void* amax,
+                        const void* bmin, const void* bmax, int64_t n, void* out, void* stream);
+
+/* brute_force_min / brute_force_max (query.py:571-619) on the device:
+ * all pairs, lexicographic tie-break. pts: device (m, 3, 3) in precision. */
+int gd_brute_force(int kind, int precision, const void* pts_a, int64_t ma, const void* pts_b,
+                   int64_t mb, GdResult* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GDIST_H */

@@ -1,0 +1,164 @@
+"""paper_2411_11244_b200: B200-native gDist (arXiv 2411.11244).
+
+Drop-in for the reference package `meshdist` (pkg/src/meshdist/__init__.py:
+8-95): the same public names with the same signatures, computed by
+hand-written sm_100a CUDA kernels in libgdist.so (csrc/) behind a C ABI
+(include/gdist.h).  `import paper_2411_11244_b200 as meshdist` is the
+intended switch.  Extra entry points named by BASELINE.json:
+`min_distance` / `max_distance(mesh_a, mesh_b, transform)`.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+from .bounds import (
+    aabb_max_upper,
+    aabb_min_lower,
+    batch_enhanced_max_lower,
+    batch_enhanced_min_upper,
+    batch_max_upper,
+    batch_min_lower,
+    batch_tri_tri_max,
+    batch_tri_tri_min,
+    enhanced_max_lower,
+    enhanced_min_upper,
+    tri_tri_max,
+    tri_tri_min,
+)
+from .bvh import Aabb, F12Bvh, build_f12, descendant, morton_codes, node_level, refit, remaining_depth
+from .errors import (
+    ConfigError,
+    DegenerateTriangleError,
+    FrontOverflowError,
+    MeshDistError,
+    ObjParseError,
+    SceneError,
+    SizeGuardError,
+    TightnessError,
+    TopologyMismatchError,
+)
+from .mesh import RigidTransform, TriangleMesh, apply_transform, load_obj
+from .query import (
+    EngineConfig,
+    Front,
+    FrontEntry,
+    IterationStat,
+    PreparedQuery,
+    QueryResult,
+    QueryState,
+    Witness,
+    adaptive_depth,
+    brute_force_max,
+    brute_force_min,
+    expand_front,
+    process_leaf_pair,
+    run_dfs_baseline,
+    run_max_query,
+    run_min_query,
+)
+from .scenes import gen_scene, ring_frame_transforms, ring_pair_base, scene_kinds, torus_mesh
+
+__version__ = "0.1.0"
+
+# one tree per (base mesh, precision), reused across calls and refit per call
+_TREES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def _tree_for(mesh: TriangleMesh, precision: int) -> F12Bvh:
+    root = mesh._root
+    per = _TREES.setdefault(root, {})
+    tree = per.get(precision)
+    if tree is None:
+        import numpy as np
+
+        tree = build_f12(root, dtype=np.float32 if precision == 32 else np.float64)
+        per[precision] = tree
+    tree.ensure_device(mesh)
+    return tree
+
+
+def _distance(kind, mesh_a, mesh_b, transform, cfg):
+    cfg = cfg or EngineConfig()
+    a = mesh_a if transform is None else apply_transform(mesh_a, transform)
+    ta = _tree_for(a, cfg.precision)
+    tb = _tree_for(mesh_b, cfg.precision)
+    res = (run_min_query if kind == "min" else run_max_query)(a, mesh_b, ta, tb, cfg)
+    pair = None if res.witness is None else (res.witness.tri_a, res.witness.tri_b)
+    return res.distance, pair
+
+
+def min_distance(mesh_a: TriangleMesh, mesh_b: TriangleMesh, transform: RigidTransform | None = None,
+                 cfg: EngineConfig | None = None):
+    """Exact minimum distance between `transform(mesh_a)` and `mesh_b`;
+    returns (distance, (tri_a, tri_b)).  Trees are built once per mesh and
+    refit on the device for every new transform."""
+    return _distance("min", mesh_a, mesh_b, transform, cfg)
+
+
+def max_distance(mesh_a: TriangleMesh, mesh_b: TriangleMesh, transform: RigidTransform | None = None,
+                 cfg: EngineConfig | None = None):
+    """Exact maximum distance between `transform(mesh_a)` and `mesh_b`;
+    returns (distance, (tri_a, tri_b))."""
+    return _distance("max", mesh_a, mesh_b, transform, cfg)
+
+
+__all__ = [
+    "Aabb",
+    "ConfigError",
+    "DegenerateTriangleError",
+    "EngineConfig",
+    "F12Bvh",
+    "Front",
+    "FrontEntry",
+    "FrontOverflowError",
+    "IterationStat",
+    "MeshDistError",
+    "ObjParseError",
+    "PreparedQuery",
+    "QueryResult",
+    "QueryState",
+    "RigidTransform",
+    "SceneError",
+    "SizeGuardError",
+    "TightnessError",
+    "TopologyMismatchError",
+    "TriangleMesh",
+    "Witness",
+    "aabb_max_upper",
+    "aabb_min_lower",
+    "adaptive_depth",
+    "apply_transform",
+    "batch_enhanced_max_lower",
+    "batch_enhanced_min_upper",
+    "batch_max_upper",
+    "batch_min_lower",
+    "batch_tri_tri_max",
+    "batch_tri_tri_min",
+    "brute_force_max",
+    "brute_force_min",
+    "build_f12",
+    "descendant",
+    "enhanced_max_lower",
+    "enhanced_min_upper",
+    "expand_front",
+    "gen_scene",
+    "load_obj",
+    "max_distance",
+    "min_distance",
+    "morton_codes",
+    "node_level",
+    "process_leaf_pair",
+    "refit",
+    "remaining_depth",
+    "ring_frame_transforms",
+    "ring_pair_base",
+    "run_dfs_baseline",
+    "run_max_query",
+    "run_min_query",
+    "scene_kinds",
+    "torus_mesh",
+    "tri_tri_max",
+    "tri_tri_min",
+    "__version__",
+]

@@ -1,0 +1,113 @@
+// engine.cuh -- shared definitions of the front-traversal engine.
+#pragma once
+
+#include "geometry.cuh"
+
+namespace gd {
+
+constexpr int kMaxIters = 64;
+
+// Device-resident query state (lives at the start of the workspace).
+struct alignas(16) QState {
+  Key128 best;                       // exact (distance, tri_a, tri_b) key
+  unsigned int bound_bits;           // float32 bits of the slack-carrying bound
+  unsigned int done;                 // last-block-done counter
+  int err;
+  int cur;                           // input front buffer (0/1)
+  int depth_a, depth_b;
+  int iter;
+  int leaf_buf;                      // buffer holding the leaf-pair list
+  unsigned long long n_in, n_out, n_leaf, n_band;
+  unsigned long long expanded, narrow, culled, band_eval;
+  long long ov_cand, ov_in, ov_cap;
+  float slack;
+  int band_overflow;
+  GdIterStat stats[kMaxIters];
+};
+
+struct QArgs {
+  GdMesh ma, mb;
+  GdBvh A, B;
+  GdConfig cfg;
+  QState* S;
+  uint2* node[2];
+  float* key[2];
+  uint2* band_ids;
+  float* band_d;
+  unsigned long long cap;       // front / leaf-list capacity (entries)
+  unsigned long long band_cap;  // band capacity (entries)
+  GdResult* result;             // device result record
+};
+
+// 24-byte AoS node box: (minx,miny,minz,maxx,maxy,maxz), float2-aligned.
+__device__ __forceinline__ Box load_box(const float* __restrict__ box, unsigned long long node) {
+  const float2* p = reinterpret_cast<const float2*>(box + node * 6);
+  float2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+  Box r;
+  r.lo[0] = a.x; r.lo[1] = a.y; r.lo[2] = b.x;
+  r.hi[0] = b.y; r.hi[1] = c.x; r.hi[2] = c.y;
+  return r;
+}
+__device__ __forceinline__ void store_box(float* box, unsigned long long node, const Box& r) {
+  float2* p = reinterpret_cast<float2*>(box + node * 6);
+  p[0] = make_float2(r.lo[0], r.lo[1]);
+  p[1] = make_float2(r.lo[2], r.hi[0]);
+  p[2] = make_float2(r.hi[1], r.hi[2]);
+}
+__device__ __forceinline__ Box box_union(const Box& a, const Box& b) {
+  Box r;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    r.lo[k] = fminf(a.lo[k], b.lo[k]);
+    r.hi[k] = fmaxf(a.hi[k], b.hi[k]);
+  }
+  return r;
+}
+
+// float32 triangle of a leaf slot: {v0, v1, v2, id} -> three vertices
+__device__ __forceinline__ Tri<float> load_tri32(const GdBvh& T, const int4& s) {
+  const float4* v = reinterpret_cast<const float4*>(T.vtx32);
+  float4 a = __ldg(v + s.x), b = __ldg(v + s.y), c = __ldg(v + s.z);
+  Tri<float> t;
+  t.v[0] = {a.x, a.y, a.z};
+  t.v[1] = {b.x, b.y, b.z};
+  t.v[2] = {c.x, c.y, c.z};
+  return t;
+}
+
+// float64 vertex of a mesh with its rigid transform applied (mesh.py:102-105)
+__device__ __forceinline__ V3<double> mesh_vertex(const GdMesh& m, long long i) {
+  const double* p = m.vtx + 3 * i;
+  double x = p[0], y = p[1], z = p[2];
+  if (!m.has_xf) return {x, y, z};
+  const double* R = m.rot;
+  using E = Exact<double>;
+  return {E::add(E::add(E::add(E::mul(R[0], x), E::mul(R[1], y)), E::mul(R[2], z)), m.trans[0]),
+          E::add(E::add(E::add(E::mul(R[3], x), E::mul(R[4], y)), E::mul(R[5], z)), m.trans[1]),
+          E::add(E::add(E::add(E::mul(R[6], x), E::mul(R[7], y)), E::mul(R[8], z)), m.trans[2])};
+}
+
+template <typename T>
+__device__ __forceinline__ Tri<T> mesh_tri(const GdMesh& m, long long t) {
+  const int32_t* ix = m.tri + 3 * t;
+  Tri<T> r;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    V3<double> v = mesh_vertex(m, ix[c]);
+    r.v[c] = {T(v.x), T(v.y), T(v.z)};  // cast-then-gather (mesh.py:64-66)
+  }
+  return r;
+}
+
+// adaptive_depth (query.py:266-284)
+__device__ __forceinline__ int adaptive_k(unsigned long long n, long long front_cap, int depth_cap,
+                                          int max_remaining) {
+  int k = 1;
+  while (k < depth_cap && k < max_remaining && (unsigned long long)(n << (2 * (k + 1))) <
+                                                   (unsigned long long)front_cap &&
+         2 * (k + 1) < 64 && (n >> (62 - 2 * (k + 1))) == 0)
+    ++k;
+  return k;
+}
+
+}  // namespace gd

@@ -1,0 +1,168 @@
+// refit.cu -- per-frame refit (bvh.py:242-306) fused with apply_transform
+// (mesh.py:102-105).
+//
+//   k_xform        float64 base vertex -> R v + t -> float32 vertex (16 B)
+//   k_leaf_up      leaf box = union of its 1..2 triangles, then the block
+//                  folds its 256-leaf subtree 8 levels up in shared memory
+//   k_level_up     the same fold for the remaining top levels
+// Every node box is written exactly once; no level is re-read from HBM
+// except the <= 1/256 subtree roots handed from one fold to the next.
+#include <algorithm>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace gd {
+
+constexpr int kFold = 256;  // nodes per block per fold (8 levels)
+
+__global__ __launch_bounds__(256) void k_xform(GdMesh m, float4* __restrict__ out) {
+  const long long i = blockIdx.x * 256ll + threadIdx.x;
+  if (i >= m.nv) return;
+  V3<double> v = mesh_vertex(m, i);
+  out[i] = make_float4((float)v.x, (float)v.y, (float)v.z, 0.f);
+}
+
+__device__ __forceinline__ Box tri_box32(const GdBvh& T, const int4& s) {
+  Tri<float> t = load_tri32(T, s);
+  Box b;
+  b.lo[0] = fminf(fminf(t.v[0].x, t.v[1].x), t.v[2].x);
+  b.lo[1] = fminf(fminf(t.v[0].y, t.v[1].y), t.v[2].y);
+  b.lo[2] = fminf(fminf(t.v[0].z, t.v[1].z), t.v[2].z);
+  b.hi[0] = fmaxf(fmaxf(t.v[0].x, t.v[1].x), t.v[2].x);
+  b.hi[1] = fmaxf(fmaxf(t.v[0].y, t.v[1].y), t.v[2].y);
+  b.hi[2] = fmaxf(fmaxf(t.v[0].z, t.v[1].z), t.v[2].z);
+  return b;
+}
+
+// fold `levels` levels inside the block; sb holds blockDim.x boxes of level
+// `lv`, the block covering nodes [first_rank, first_rank + blockDim.x)
+__device__ __forceinline__ void fold_up(float* box, Box* sb, Box mine, int lv, long long first_rank,
+                                        int levels) {
+  int width = blockDim.x;
+  sb[threadIdx.x] = mine;
+  for (int u = 0; u < levels; ++u) {
+    __syncthreads();
+    width >>= 1;
+    Box p;
+    const bool act = threadIdx.x < width;
+    if (act) p = box_union(sb[2 * threadIdx.x], sb[2 * threadIdx.x + 1]);
+    __syncthreads();
+    --lv;
+    first_rank >>= 1;
+    if (act) {
+      sb[threadIdx.x] = p;
+      store_box(box, ((1ull << lv) - 1) + first_rank + threadIdx.x, p);
+    }
+  }
+}
+
+__global__ __launch_bounds__(kFold) void k_leaf_up(GdBvh T, int levels) {
+  __shared__ Box sb[kFold];
+  const long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // leaf rank (< L exactly)
+  const int4* lt = reinterpret_cast<const int4*>(T.leaf_tri);
+  const unsigned f0 = T.leaf_first[l], f1 = T.leaf_first[l + 1];
+  Box b = tri_box32(T, __ldg(lt + f0));
+  if (f1 - f0 == 2) b = box_union(b, tri_box32(T, __ldg(lt + f0 + 1)));
+  store_box(T.box, (T.leaf_count - 1) + l, b);
+  fold_up(T.box, sb, b, T.depth, blockIdx.x * (long long)blockDim.x, levels);
+}
+
+__global__ __launch_bounds__(kFold) void k_level_up(float* box, int lv, int levels) {
+  __shared__ Box sb[kFold];
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  Box b = load_box(box, ((1ull << lv) - 1) + r);
+  fold_up(box, sb, b, lv, blockIdx.x * (long long)blockDim.x, levels);
+}
+
+void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
+  GD_CHECK(m.m == T.n_tris, GD_ERR_TOPOLOGY,
+           "refit mesh has " + std::to_string(m.m) + " triangles, tree was built over " + std::to_string(T.n_tris));
+  GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "refit mesh vertex count differs from the build");
+  long long launches = 0;
+  if (m.nv > 0) {
+    k_xform<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, reinterpret_cast<float4*>(T.vtx32));
+    ++launches;
+  }
+  const long long L = T.leaf_count;
+  int lv = T.depth;
+  const int bs = (int)std::min<long long>(L, kFold);
+  const int lev = std::min(lv, __builtin_ctz((unsigned)bs));
+  k_leaf_up<<<(unsigned)(L / bs), bs, 0, s>>>(T, lev);
+  ++launches;
+  lv -= lev;
+  while (lv > 0) {
+    const long long cnt = 1ll << lv;
+    const int b2 = (int)std::min<long long>(cnt, kFold);
+    const int l2 = std::min(lv, __builtin_ctz((unsigned)b2));
+    k_level_up<<<(unsigned)(cnt / b2), b2, 0, s>>>(T.box, lv, l2);
+    ++launches;
+    lv -= l2;
+  }
+  GD_CUDA(cudaGetLastError());
+  count_launches(launches);
+}
+
+// ---------------------------------------------------------------------------
+// node boxes with the reference's dtype semantics (bvh.py:242-264): the
+// float64 path reads the float64 vertices, the float32 path casts first.
+template <typename T>
+__global__ void k_export_leaf(GdMesh m, GdBvh B, T* nmin, T* nmax) {
+  const long long l = blockIdx.x * 256ll + threadIdx.x;
+  if (l >= B.leaf_count) return;
+  const int4* lt = reinterpret_cast<const int4*>(B.leaf_tri);
+  const unsigned f0 = B.leaf_first[l], f1 = B.leaf_first[l + 1];
+  T lo[3], hi[3];
+  for (unsigned f = f0; f < f1; ++f) {
+    const int4 s = lt[f];
+    const int v[3] = {s.x, s.y, s.z};
+    for (int c = 0; c < 3; ++c) {
+      V3<double> p = mesh_vertex(m, v[c]);
+      T x[3] = {T(p.x), T(p.y), T(p.z)};
+      for (int k = 0; k < 3; ++k) {
+        if (f == f0 && c == 0) {
+          lo[k] = hi[k] = x[k];
+        } else {
+          lo[k] = x[k] < lo[k] ? x[k] : lo[k];
+          hi[k] = x[k] > hi[k] ? x[k] : hi[k];
+        }
+      }
+    }
+  }
+  const long long node = (B.leaf_count - 1) + l;
+  for (int k = 0; k < 3; ++k) {
+    nmin[3 * node + k] = lo[k];
+    nmax[3 * node + k] = hi[k];
+  }
+}
+
+template <typename T>
+__global__ void k_export_level(T* nmin, T* nmax, int lv) {
+  const long long r = blockIdx.x * 256ll + threadIdx.x;
+  if (r >= (1ll << lv)) return;
+  const long long node = ((1ll << lv) - 1) + r, c0 = 2 * node + 1, c1 = c0 + 1;
+  for (int k = 0; k < 3; ++k) {
+    const T a = nmin[3 * c0 + k], b = nmin[3 * c1 + k];
+    nmin[3 * node + k] = b < a ? b : a;  // np.minimum
+    const T c = nmax[3 * c0 + k], d = nmax[3 * c1 + k];
+    nmax[3 * node + k] = d > c ? d : c;  // np.maximum
+  }
+}
+
+void export_boxes(const GdMesh& m, const GdBvh& B, int precision, void* nmin, void* nmax, cudaStream_t s) {
+  GD_CHECK(precision == 32 || precision == 64, GD_ERR_CONFIG, "precision must be 32 or 64");
+  const unsigned g = (unsigned)((B.leaf_count + 255) / 256);
+  if (precision == 64) {
+    k_export_leaf<double><<<g, 256, 0, s>>>(m, B, (double*)nmin, (double*)nmax);
+    for (int lv = B.depth - 1; lv >= 0; --lv)
+      k_export_level<double><<<(unsigned)(((1ll << lv) + 255) / 256), 256, 0, s>>>((double*)nmin, (double*)nmax, lv);
+  } else {
+    k_export_leaf<float><<<g, 256, 0, s>>>(m, B, (float*)nmin, (float*)nmax);
+    for (int lv = B.depth - 1; lv >= 0; --lv)
+      k_export_level<float><<<(unsigned)(((1ll << lv) + 255) / 256), 256, 0, s>>>((float*)nmin, (float*)nmax, lv);
+  }
+  GD_CUDA(cudaGetLastError());
+  GD_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace gd

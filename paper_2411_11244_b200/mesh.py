@@ -1,0 +1,229 @@
+"""Triangle meshes, rigid motion and OBJ ingest (reference mesh.py:21-163).
+
+`TriangleMesh` keeps the reference's host contract (float64 / int64
+read-only arrays, same validation errors) and adds a device view: the base
+vertices are uploaded once and cached on the object.  `apply_transform` is
+lazy on the device: the moved mesh shares the base upload and carries the
+composed rigid transform, which the refit and exact kernels apply on the fly
+(no per-frame vertex upload).  Reading `.vertices` of a moved mesh
+materialises it on the host with the reference's own formula
+(`V @ R.T + t`, applied transform by transform), bit for bit.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+from . import _lib
+from .errors import DegenerateTriangleError, ObjParseError
+
+_IDENTITY = np.eye(3)
+
+
+def _validated(vertices, triangles):
+    verts = np.ascontiguousarray(np.asarray(vertices, dtype=np.float64))
+    tris = np.ascontiguousarray(np.asarray(triangles, dtype=np.int64))
+    if verts.ndim != 2 or verts.shape[1] != 3:
+        raise ValueError(f"vertices must be (n, 3), got {verts.shape}")
+    if tris.size == 0:
+        tris = tris.reshape(0, 3)
+    if tris.ndim != 2 or tris.shape[1] != 3:
+        raise ValueError(f"triangles must be (m, 3), got {tris.shape}")
+    if tris.size:
+        if tris.min() < 0 or tris.max() >= len(verts):
+            raise ValueError("triangle index out of range")
+        bad = (tris[:, 0] == tris[:, 1]) | (tris[:, 1] == tris[:, 2]) | (tris[:, 0] == tris[:, 2])
+        if bad.any():
+            raise DegenerateTriangleError([(int(i), tuple(int(v) for v in tris[i])) for i in np.flatnonzero(bad)])
+    verts.setflags(write=False)
+    tris.setflags(write=False)
+    return verts, tris
+
+
+class TriangleMesh:
+    """Immutable indexed triangle soup (mesh.py:21-66).
+
+    vertices: (n, 3) float64, triangles: (m, 3) int64, both read-only."""
+
+    __slots__ = ("_vertices", "_triangles", "_root", "_chain", "_rot", "_trans", "_dev", "__weakref__")
+
+    def __init__(self, vertices, triangles):
+        self._vertices, self._triangles = _validated(vertices, triangles)
+        self._root = self
+        self._chain = ()          # host transforms still to apply to root.vertices
+        self._rot = None          # composed device transform (None = identity)
+        self._trans = None
+        self._dev = None
+
+    # -- lazily moved mesh (apply_transform) ------------------------------
+    @classmethod
+    def _moved(cls, src: "TriangleMesh", xf: "RigidTransform") -> "TriangleMesh":
+        out = cls.__new__(cls)
+        out._vertices = None
+        out._triangles = src._triangles
+        out._root = src._root
+        out._chain = src._chain + (xf,)
+        R0 = _IDENTITY if src._rot is None else src._rot
+        t0 = np.zeros(3) if src._trans is None else src._trans
+        out._rot = xf.rotation @ R0
+        out._trans = xf.rotation @ t0 + xf.translation
+        out._dev = None
+        return out
+
+    @property
+    def vertices(self) -> np.ndarray:
+        if self._vertices is None:
+            v = self._root._vertices
+            for xf in self._chain:
+                v = v @ xf.rotation.T + xf.translation  # mesh.py:104, transform by transform
+            v = np.ascontiguousarray(v)
+            v.setflags(write=False)
+            self._vertices = v
+        return self._vertices
+
+    @property
+    def triangles(self) -> np.ndarray:
+        return self._triangles
+
+    @property
+    def n_triangles(self) -> int:
+        return len(self._triangles)
+
+    @property
+    def n_vertices(self) -> int:
+        return len(self._root._vertices)
+
+    def triangle_points(self, dtype=np.float64) -> np.ndarray:
+        """(m, 3, 3) corners: cast first, then gather (mesh.py:64-66)."""
+        return self.vertices.astype(dtype, copy=False)[self._triangles]
+
+    def __repr__(self) -> str:
+        return f"TriangleMesh(n_vertices={self.n_vertices}, n_triangles={self.n_triangles})"
+
+    # -- device view --------------------------------------------------------
+    def _upload(self):
+        """Upload the root's float64 vertices and int32 indices once."""
+        root = self._root
+        if root._dev is None:
+            torch = _lib.torch()
+            dev = _lib.device()
+            if len(root._triangles) >= 2**31 or len(root._vertices) >= 2**31:
+                raise ValueError("meshes above 2^31 vertices/triangles are not supported")
+            vt = torch.from_numpy(np.ascontiguousarray(root._vertices)).to(dev)
+            tr = torch.from_numpy(root._triangles.astype(np.int32)).to(dev)
+            root._dev = (vt, tr)
+        return root._dev
+
+    def device_view(self) -> _lib.GdMesh:
+        vt, tr = self._upload()
+        g = _lib.GdMesh()
+        g.vtx = vt.data_ptr()
+        g.tri = tr.data_ptr()
+        g.nv = vt.shape[0]
+        g.m = tr.shape[0]
+        if self._rot is None:
+            g.rot[:] = [1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0]
+            g.trans[:] = [0.0, 0.0, 0.0]
+            g.has_xf = 0
+        else:
+            g.rot[:] = [float(x) for x in self._rot.reshape(9)]
+            g.trans[:] = [float(x) for x in self._trans.reshape(3)]
+            g.has_xf = 1
+        return g
+
+    def _geometry_key(self):
+        """Identity of the geometry the device sees (root + transform)."""
+        if self._rot is None:
+            return (id(self._root), None)
+        return (id(self._root), self._rot.tobytes() + self._trans.tobytes())
+
+
+class RigidTransform:
+    """Rotation (3x3 orthonormal within 1e-6) then translation (mesh.py:69-99)."""
+
+    __slots__ = ("rotation", "translation")
+
+    def __init__(self, rotation=None, translation=None):
+        rot = np.asarray(np.eye(3) if rotation is None else rotation, dtype=np.float64).reshape(3, 3).copy()
+        t = np.asarray(np.zeros(3) if translation is None else translation, dtype=np.float64).reshape(3).copy()
+        if not np.allclose(rot @ rot.T, np.eye(3), atol=1e-6):
+            raise ValueError("rotation matrix is not orthonormal within 1e-6")
+        rot.setflags(write=False)
+        t.setflags(write=False)
+        object.__setattr__(self, "rotation", rot)
+        object.__setattr__(self, "translation", t)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("RigidTransform is immutable")
+
+    @classmethod
+    def from_axis_angle(cls, axis, angle_rad: float, translation=(0.0, 0.0, 0.0)) -> "RigidTransform":
+        """Rodrigues: c I + s [a]x + (1 - c) a a^T (mesh.py:86-99)."""
+        a = np.asarray(axis, dtype=np.float64)
+        n = np.linalg.norm(a)
+        if n == 0.0:
+            raise ValueError("rotation axis must be nonzero")
+        a = a / n
+        c, s = math.cos(angle_rad), math.sin(angle_rad)
+        skew = np.array([[0.0, -a[2], a[1]], [a[2], 0.0, -a[0]], [-a[1], a[0], 0.0]])
+        rot = c * np.eye(3) + s * skew + (1.0 - c) * np.outer(a, a)
+        return cls(rotation=rot, translation=np.asarray(translation, dtype=np.float64))
+
+    def compose(self, inner: "RigidTransform") -> "RigidTransform":
+        """self o inner: v -> R_self (R_inner v + t_inner) + t_self."""
+        return RigidTransform(self.rotation @ inner.rotation, self.rotation @ inner.translation + self.translation)
+
+    def __repr__(self) -> str:
+        return f"RigidTransform(rotation={self.rotation.tolist()}, translation={self.translation.tolist()})"
+
+
+def apply_transform(mesh: TriangleMesh, xf: RigidTransform) -> TriangleMesh:
+    """Map every vertex v to R v + t; topology shared (mesh.py:102-105).
+    O(1): the device applies the transform inside refit / the exact pass."""
+    return TriangleMesh._moved(mesh, xf)
+
+
+def load_obj(path) -> TriangleMesh:
+    """Wavefront OBJ subset: `v`, `f` (fan-triangulated, negative indices
+    relative), `#` comments; everything else ignored (mesh.py:108-163)."""
+    path = os.fspath(path)
+    verts: list = []
+    faces: list = []
+    with open(path, "r", encoding="utf-8", errors="replace") as fh:
+        for line_no, raw in enumerate(fh, start=1):
+            body = raw.split("#", 1)[0].strip()
+            if not body:
+                continue
+            tok = body.split()
+            if tok[0] == "v":
+                if len(tok) < 4:
+                    raise ObjParseError(path, line_no, "vertex needs 3 coordinates")
+                try:
+                    verts.append((float(tok[1]), float(tok[2]), float(tok[3])))
+                except ValueError as exc:
+                    raise ObjParseError(path, line_no, f"bad vertex coordinate: {exc}") from None
+            elif tok[0] == "f":
+                if len(tok) < 4:
+                    raise ObjParseError(path, line_no, "face needs at least 3 vertices")
+                idx = []
+                for item in tok[1:]:
+                    head = item.split("/", 1)[0]
+                    try:
+                        ref = int(head)
+                    except ValueError:
+                        raise ObjParseError(path, line_no, f"bad face index {item!r}") from None
+                    if ref == 0:
+                        raise ObjParseError(path, line_no, "face index 0 is not valid OBJ")
+                    k = ref - 1 if ref > 0 else len(verts) + ref
+                    if k < 0 or k >= len(verts):
+                        raise ObjParseError(path, line_no, f"face index {ref} out of range (have {len(verts)} vertices)")
+                    idx.append(k)
+                faces.extend((idx[0], idx[i], idx[i + 1]) for i in range(1, len(idx) - 1))
+    return TriangleMesh(
+        np.asarray(verts, dtype=np.float64).reshape(len(verts), 3),
+        np.asarray(faces, dtype=np.int64).reshape(len(faces), 3),
+    )

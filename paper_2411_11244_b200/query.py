@@ -1,0 +1,495 @@
+"""Front-traversal distance queries on the device (reference query.py).
+
+`run_min_query` / `run_max_query` run the whole BVTT traversal -- adaptive
+depth, expansion with AABB culling, float32 narrow phase, exact pass -- as a
+fixed launch sequence inside libgdist (csrc/query.cu) with one device->host
+copy at the end.  The returned distance is the reference's exact value (its
+float64 or float32 arithmetic, per `precision`), and the witness is the
+lexicographically smallest (tri_a, tri_b) pair attaining it, i.e. the
+brute-force witness (query.py:571-601).  See DESIGN.md "Exactness".
+
+The single-step API (`expand_front`, `process_leaf_pair`, `QueryState`) is
+kept with the reference's semantics; its arithmetic runs in libgdist's exact
+batch kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .bounds import _device_bounds, _device_tri_tri
+from .bvh import F12Bvh
+from .errors import ConfigError, FrontOverflowError, SizeGuardError
+from .mesh import TriangleMesh
+
+BRUTE_FORCE_PAIR_LIMIT = 10_000_000  # query.py:48
+
+
+@dataclass(frozen=True)
+class EngineConfig:
+    """Engine knobs (query.py:51-102).  `threads` and `batch_size` are
+    accepted for compatibility; the device engine has no use for them."""
+
+    front_cap: int = 262_144
+    depth_cap: int = 5
+    precision: int = 64
+    threads: int | str = 1
+    enhanced_bounds: bool = True
+    culling: bool = True
+    guarantee_witness: bool = False
+    front_hard_cap: int = 16_777_216
+    batch_size: int = 65_536
+
+    def __post_init__(self):
+        if self.front_cap < 4:
+            raise ConfigError(f"front_cap must be >= 4, got {self.front_cap}")
+        if not 1 <= self.depth_cap <= 16:
+            raise ConfigError(f"depth_cap must be in [1, 16], got {self.depth_cap}")
+        if self.precision not in (32, 64):
+            raise ConfigError(f"precision must be 32 or 64, got {self.precision}")
+        if self.batch_size < 4:
+            raise ConfigError(f"batch_size must be >= 4, got {self.batch_size}")
+        if self.front_hard_cap < 4:
+            raise ConfigError("front_hard_cap must be >= 4")
+        if isinstance(self.threads, str):
+            if self.threads != "auto":
+                raise ConfigError(f"threads must be a positive int or 'auto', got {self.threads!r}")
+        elif self.threads < 1:
+            raise ConfigError(f"threads must be >= 1, got {self.threads}")
+
+    @property
+    def dtype(self):
+        return np.float32 if self.precision == 32 else np.float64
+
+    @property
+    def worker_count(self) -> int:
+        if self.threads == "auto":
+            return os.cpu_count() or 1
+        return int(self.threads)
+
+
+@dataclass(frozen=True)
+class FrontEntry:
+    """One unresolved node pair with its cached culling key (query.py:105-113)."""
+
+    node_a: int
+    node_b: int
+    lower: float
+
+
+@dataclass
+class Front:
+    """A front as flat arrays at one depth pair (query.py:116-133)."""
+
+    node_a: np.ndarray
+    node_b: np.ndarray
+    lower: np.ndarray
+    depth_a: int
+    depth_b: int
+
+    def __len__(self) -> int:
+        return len(self.node_a)
+
+    def entries(self) -> list:
+        return [FrontEntry(int(a), int(b), float(lo)) for a, b, lo in zip(self.node_a, self.node_b, self.lower)]
+
+
+@dataclass(frozen=True)
+class Witness:
+    """Triangle pair (and points on them) attaining a distance (query.py:136-144)."""
+
+    distance: float
+    tri_a: int
+    tri_b: int
+    point_a: np.ndarray
+    point_b: np.ndarray
+
+
+@dataclass(frozen=True)
+class IterationStat:
+    k: int
+    front_in: int
+    front_out: int
+    culled: int
+    bound_after: float
+
+    def to_json_dict(self) -> dict:
+        return {"k": self.k, "front_in": self.front_in, "front_out": self.front_out, "culled": self.culled,
+                "bound_after": self.bound_after}
+
+
+class QueryState:
+    """Monotone bound + lexicographic witness cell (query.py:165-227)."""
+
+    def __init__(self, kind: str, bound: float):
+        if kind not in ("min", "max"):
+            raise ValueError(f"kind must be 'min' or 'max', got {kind!r}")
+        self.kind = kind
+        self._bound = float(bound)
+        self._witness = None
+        self._lock = threading.Lock()
+        self.iterations: list = []
+        self.expanded_pairs = 0
+        self.narrow_pairs = 0
+
+    @property
+    def bound(self) -> float:
+        with self._lock:
+            return self._bound
+
+    def offer_bound(self, value: float) -> None:
+        value = float(value)
+        with self._lock:
+            if (value < self._bound) if self.kind == "min" else (value > self._bound):
+                self._bound = value
+
+    @property
+    def witness(self):
+        with self._lock:
+            return self._witness
+
+    def offer_witness(self, distance: float, tri_a: int, tri_b: int, point_a, point_b) -> None:
+        distance = float(distance)
+        with self._lock:
+            w = self._witness
+            if w is None:
+                better = True
+            else:
+                better = distance < w.distance if self.kind == "min" else distance > w.distance
+                if not better and distance == w.distance:
+                    better = (tri_a, tri_b) < (w.tri_a, w.tri_b)
+            if better:
+                self._witness = Witness(distance, int(tri_a), int(tri_b), np.array(point_a), np.array(point_b))
+
+    def add_narrow_pairs(self, n: int) -> None:
+        with self._lock:
+            self.narrow_pairs += n
+
+    def record_iteration(self, k: int, front_in: int, front_out: int, culled: int) -> None:
+        self.iterations.append(IterationStat(k, front_in, front_out, culled, self.bound))
+
+
+@dataclass(frozen=True)
+class QueryResult:
+    """query.py:230-263; `band_pairs` counts exact-pass evaluations."""
+
+    kind: str
+    distance: float
+    witness: Witness | None
+    iterations: tuple
+    expanded_pairs: int
+    narrow_pairs: int
+    visited_nodes: int | None = None
+    band_pairs: int = field(default=0, compare=False)
+
+    @property
+    def witness_exact(self) -> bool:
+        return self.witness is not None and self.witness.distance == self.distance
+
+    @property
+    def peak_front(self) -> int:
+        return max((s.front_out for s in self.iterations), default=0)
+
+    def to_json_dict(self) -> dict:
+        w = self.witness
+        return {
+            "kind": self.kind,
+            "distance": self.distance,
+            "witness_exact": self.witness_exact,
+            "tri_a": None if w is None else w.tri_a,
+            "tri_b": None if w is None else w.tri_b,
+            "point_a": None if w is None else [float(x) for x in w.point_a],
+            "point_b": None if w is None else [float(x) for x in w.point_b],
+            "iterations": [s.to_json_dict() for s in self.iterations],
+            "expanded_pairs": self.expanded_pairs,
+            "narrow_pairs": self.narrow_pairs,
+            "peak_front": self.peak_front,
+            "visited_nodes": self.visited_nodes,
+        }
+
+
+def adaptive_depth(n: int, cfg: EngineConfig, max_remaining: int) -> int:
+    """Largest k with 4^k n < C, clamped to [1, min(depth_cap, max_remaining)]
+    (query.py:266-284)."""
+    if n < 1:
+        raise ValueError("front size must be >= 1")
+    if max_remaining < 1:
+        raise ValueError("max_remaining must be >= 1")
+    k = 1
+    while k < cfg.depth_cap and k < max_remaining and (n << (2 * (k + 1))) < cfg.front_cap:
+        k += 1
+    return k
+
+
+# ---------------------------------------------------------------------------
+# device engine
+# ---------------------------------------------------------------------------
+_MAX_STATS = 64
+
+
+class _Workspace:
+    """Per-device scratch for the query engine, grown on demand and reused."""
+
+    _cache: dict = {}
+    _lock = threading.Lock()
+
+    @classmethod
+    def get(cls, nbytes: int):
+        torch = _lib.torch()
+        dev = torch.cuda.current_device()
+        with cls._lock:
+            t = cls._cache.get(dev)
+            if t is None or t.numel() < nbytes:
+                cls._cache.pop(dev, None)
+                t = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", dev))
+                cls._cache[dev] = t
+            return t
+
+
+def _gd_config(cfg: EngineConfig, kind: str, warm_pair, band_cap: int = 0) -> _lib.GdConfig:
+    g = _lib.GdConfig()
+    g.kind = 1 if kind == "max" else 0
+    g.precision = cfg.precision
+    g.front_cap = cfg.front_cap
+    g.depth_cap = cfg.depth_cap
+    g.enhanced_bounds = int(bool(cfg.enhanced_bounds))
+    g.culling = int(bool(cfg.culling))
+    g.guarantee_witness = int(bool(cfg.guarantee_witness))
+    g.front_hard_cap = cfg.front_hard_cap
+    if warm_pair is not None:
+        g.warm_a, g.warm_b = int(warm_pair[0]), int(warm_pair[1])
+    else:
+        g.warm_a = g.warm_b = -1
+    g.band_cap = band_cap
+    return g
+
+
+def _check_build(cfg: EngineConfig, bvh_a: F12Bvh, bvh_b: F12Bvh) -> None:
+    """query.py:471-477."""
+    for name, bvh in (("A", bvh_a), ("B", bvh_b)):
+        if bvh.dtype != np.dtype(cfg.dtype):
+            raise ConfigError(
+                f"BVH {name} was built as {bvh.dtype}, engine precision is {cfg.precision}-bit; "
+                f"rebuild with build_f12(mesh, dtype=...) to match"
+            )
+
+
+class PreparedQuery:
+    """A query bound to its meshes / trees / config: the device views and
+    workspace are resolved once, so repeated launches (frames, benches) cost
+    only the kernel sequence.  `launch()` is asynchronous; `collect()` does
+    the single device->host copy."""
+
+    def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, cfg: EngineConfig, kind: str, warm_pair=None):
+        _check_build(cfg, bvh_a, bvh_b)
+        if warm_pair is not None:
+            ta, tb = int(warm_pair[0]), int(warm_pair[1])
+            if not (0 <= ta < mesh_a.n_triangles and 0 <= tb < mesh_b.n_triangles):
+                raise IndexError(f"warm_pair {warm_pair} out of range")
+        bvh_a.ensure_device(mesh_a)
+        bvh_b.ensure_device(mesh_b)
+        self.kind = kind
+        self.meshes = (mesh_a, mesh_b)
+        self.trees = (bvh_a, bvh_b)
+        self.g_ma, self.g_mb = mesh_a.device_view(), mesh_b.device_view()
+        self.g_a, self.g_b = bvh_a.device_view(), bvh_b.device_view()
+        self.g_cfg = _gd_config(cfg, kind, warm_pair)
+        nbytes = C.c_size_t(0)
+        L = _lib.lib()
+        _lib.check(L.gd_query_workspace_size(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg),
+                                             C.byref(nbytes)), "query_workspace_size")
+        self.ws = _Workspace.get(nbytes.value)
+        self.res = _lib.GdResult()
+        self.stats = (_lib.GdIterStat * _MAX_STATS)()
+
+    def launch(self, stream=None):
+        _lib.check(_lib.lib().gd_query_async(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a),
+                                             C.byref(self.g_b), C.byref(self.g_cfg), _lib.ptr(self.ws),
+                                             self.ws.numel(), None, stream or _lib.stream_ptr()), "query")
+
+    def collect(self, stream=None) -> QueryResult:
+        _lib.check(_lib.lib().gd_query_collect(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg),
+                                               _lib.ptr(self.ws), None, C.byref(self.res), self.stats, _MAX_STATS,
+                                               stream or _lib.stream_ptr()), "query")
+        return _result(self.kind, self.res, self.stats)
+
+    def run(self) -> QueryResult:
+        self.launch()
+        return self.collect()
+
+
+def _result(kind: str, r: _lib.GdResult, stats) -> QueryResult:
+    if r.status == _lib.GD_ERR_FRONT_OVERFLOW:
+        raise _lib.overflow_error(r)
+    if r.status != 0:
+        raise RuntimeError(f"device query failed with status {r.status}")
+    its = tuple(
+        IterationStat(int(s.k), int(s.front_in), int(s.front_out), int(s.culled), float(s.bound_after))
+        for s in stats[: min(r.iterations, _MAX_STATS)]
+    )
+    w = None
+    if r.tri_a >= 0:
+        w = Witness(float(r.witness_distance), int(r.tri_a), int(r.tri_b), np.array(r.point_a[:], dtype=np.float64),
+                    np.array(r.point_b[:], dtype=np.float64))
+    return QueryResult(kind, float(r.distance), w, its, int(r.expanded_pairs), int(r.narrow_pairs),
+                       band_pairs=int(r.band_pairs))
+
+
+def _run_query(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair=None) -> QueryResult:
+    return PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair).run()
+
+
+def run_min_query(mesh_a: TriangleMesh, mesh_b: TriangleMesh, bvh_a: F12Bvh, bvh_b: F12Bvh,
+                  cfg: EngineConfig | None = None, warm_pair=None) -> QueryResult:
+    """Exact minimum distance between two meshes (query.py:540-555)."""
+    return _run_query(mesh_a, mesh_b, bvh_a, bvh_b, cfg or EngineConfig(), "min", warm_pair)
+
+
+def run_max_query(mesh_a: TriangleMesh, mesh_b: TriangleMesh, bvh_a: F12Bvh, bvh_b: F12Bvh,
+                  cfg: EngineConfig | None = None, warm_pair=None) -> QueryResult:
+    """Exact maximum distance between two meshes (query.py:558-568)."""
+    return _run_query(mesh_a, mesh_b, bvh_a, bvh_b, cfg or EngineConfig(), "max", warm_pair)
+
+
+# ---------------------------------------------------------------------------
+# brute force (query.py:571-619) -- all pairs on the device
+# ---------------------------------------------------------------------------
+def _brute_force(mesh_a, mesh_b, kind, force, dtype):
+    na, nb = mesh_a.n_triangles, mesh_b.n_triangles
+    n_pairs = na * nb
+    if n_pairs == 0:
+        raise ValueError("both meshes need at least one triangle")
+    if n_pairs > BRUTE_FORCE_PAIR_LIMIT and not force:
+        raise SizeGuardError(n_pairs, BRUTE_FORCE_PAIR_LIMIT)
+    torch = _lib.torch()
+    dev = _lib.device()
+    prec = 32 if np.dtype(dtype) == np.float32 else 64
+    pa = torch.from_numpy(np.ascontiguousarray(mesh_a.triangle_points(dtype))).to(dev)
+    pb = torch.from_numpy(np.ascontiguousarray(mesh_b.triangle_points(dtype))).to(dev)
+    r = _lib.GdResult()
+    _lib.check(_lib.lib().gd_brute_force(1 if kind == "max" else 0, prec, _lib.ptr(pa), na, _lib.ptr(pb), nb,
+                                         C.byref(r), _lib.stream_ptr()), "brute_force")
+    w = Witness(float(r.distance), int(r.tri_a), int(r.tri_b), np.array(r.point_a[:]), np.array(r.point_b[:]))
+    return float(r.distance), w
+
+
+def brute_force_min(mesh_a, mesh_b, force: bool = False, dtype=np.float64):
+    """All-pairs exact minimum (query.py:604-612); lexicographic ties."""
+    return _brute_force(mesh_a, mesh_b, "min", force, dtype)
+
+
+def brute_force_max(mesh_a, mesh_b, force: bool = False, dtype=np.float64):
+    """All-pairs exact maximum (query.py:615-619)."""
+    return _brute_force(mesh_a, mesh_b, "max", force, dtype)
+
+
+# ---------------------------------------------------------------------------
+# single-step API with the reference's exact semantics
+# ---------------------------------------------------------------------------
+def _narrow_update(state: QueryState, ids_a, ids_b, pts_a, pts_b) -> None:
+    """query.py:287-307 with the exact device kernels."""
+    if len(ids_a) == 0:
+        return
+    d, p, q = _device_tri_tri(state.kind, pts_a[ids_a], pts_b[ids_b])
+    if state.kind == "min":
+        pick = np.lexsort((ids_b, ids_a, d))[0]
+    else:
+        pick = np.lexsort((ids_b, ids_a, -d))[0]
+    state.add_narrow_pairs(len(ids_a))
+    state.offer_bound(d[pick])
+    state.offer_witness(d[pick], ids_a[pick], ids_b[pick], p[pick].astype(np.float64), q[pick].astype(np.float64))
+
+
+def process_leaf_pair(leaf_a_prims, leaf_b_prims, mesh_a, mesh_b, state: QueryState) -> QueryState:
+    """All 1..4 triangle pairs of two leaves into the state (query.py:310-331)."""
+    ids_a = np.asarray([a for a in leaf_a_prims for _ in leaf_b_prims], dtype=np.int64)
+    ids_b = np.asarray([b for _ in leaf_a_prims for b in leaf_b_prims], dtype=np.int64)
+    _narrow_update(state, ids_a, ids_b, mesh_a.triangle_points(), mesh_b.triangle_points())
+    return state
+
+
+def _leaf_tri_pairs(bvh_a, bvh_b, na, nb):
+    ta = bvh_a.leaf_tris[na - (bvh_a.leaf_count - 1)]
+    tb = bvh_b.leaf_tris[nb - (bvh_b.leaf_count - 1)]
+    outa, outb = [], []
+    for i in (0, 1):
+        for j in (0, 1):
+            sel = (ta[:, i] >= 0) & (tb[:, j] >= 0)
+            outa.append(ta[sel, i])
+            outb.append(tb[sel, j])
+    return np.concatenate(outa), np.concatenate(outb)
+
+
+def expand_front(front: Front, k: int, state: QueryState, bvh_a: F12Bvh, bvh_b: F12Bvh, pts_a, pts_b,
+                 cfg: EngineConfig, pool=None) -> Front:
+    """One expansion sweep with the reference's batch semantics
+    (query.py:349-451); bounds and narrow phase run in the exact device
+    batch kernels, so results equal the reference's bit for bit."""
+    rem_a = bvh_a.depth - front.depth_a
+    rem_b = bvh_b.depth - front.depth_b
+    ka, kb = min(k, rem_a), min(k, rem_b)
+    shift = ka + kb
+    n_in = len(front)
+    n_candidates = n_in << shift
+    if n_candidates > cfg.front_hard_cap:
+        raise FrontOverflowError(n_candidates, n_in, cfg.front_hard_cap)
+    to_leaves = k == max(rem_a, rem_b)
+    state.expanded_pairs += n_candidates
+    mask_b = (1 << kb) - 1
+    amin_all, amax_all = bvh_a.node_min, bvh_a.node_max
+    bmin_all, bmax_all = bvh_b.node_min, bvh_b.node_max
+    is_min = state.kind == "min"
+    outs, culled_total = [], 0
+    for start in range(0, n_candidates, cfg.batch_size):
+        idx = np.arange(start, min(start + cfg.batch_size, n_candidates), dtype=np.int64)
+        e = idx >> shift
+        off = idx & ((1 << shift) - 1)
+        na = ((front.node_a[e] + 1) << ka) - 1 + (off >> kb)
+        nb = ((front.node_b[e] + 1) << kb) - 1 + (off & mask_b)
+        boxes = (amin_all[na], amax_all[na], bmin_all[nb], bmax_all[nb])
+        key = _device_bounds(0 if is_min else 1, *boxes)
+        bound = state.bound
+        if not cfg.culling:
+            keep = np.ones(len(idx), dtype=bool)
+        elif is_min:
+            keep = key <= bound if (to_leaves and cfg.guarantee_witness) else key < bound
+        else:
+            keep = key >= bound if (to_leaves and cfg.guarantee_witness) else key > bound
+        culled_total += int(len(idx) - keep.sum())
+        na, nb, key = na[keep], nb[keep], key[keep]
+        if to_leaves:
+            if len(na):
+                ia, ib = _leaf_tri_pairs(bvh_a, bvh_b, na, nb)
+                _narrow_update(state, ia, ib, pts_a, pts_b)
+            continue
+        if len(na):
+            kept = tuple(b[keep] for b in boxes)
+            which = (2 if cfg.enhanced_bounds else 1) if is_min else (3 if cfg.enhanced_bounds else 0)
+            upd = _device_bounds(which, *kept)
+            state.offer_bound(upd.min() if is_min else upd.max())
+            outs.append((na, nb, key))
+    out = Front(
+        node_a=np.concatenate([o[0] for o in outs]) if outs else np.empty(0, dtype=np.int64),
+        node_b=np.concatenate([o[1] for o in outs]) if outs else np.empty(0, dtype=np.int64),
+        lower=np.concatenate([o[2] for o in outs]) if outs else np.empty(0, dtype=np.float64),
+        depth_a=front.depth_a + ka,
+        depth_b=front.depth_b + kb,
+    )
+    if len(out) > cfg.front_hard_cap:
+        raise FrontOverflowError(len(out), n_in, cfg.front_hard_cap)
+    state.record_iteration(k, n_in, len(out), culled_total)
+    return out
+
+
+def run_dfs_baseline(mesh_a, mesh_b, bvh_b, kind: str = "min") -> QueryResult:
+    """Per-triangle DFS comparator (query.py:622-708) -- the paper's naive
+    GPU baseline; see dfs.py."""
+    from .dfs import run_dfs
+
+    return run_dfs(mesh_a, mesh_b, bvh_b, kind)

@@ -1,0 +1,67 @@
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO))
+GOLDEN = REPO / "tests" / "golden"
+REFERENCE_SRC = Path(os.environ.get("MESHDIST_REFERENCE", "/root/reference/pkg/src"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a) and libgdist.so")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture(scope="session")
+def golden():
+    return np.load(GOLDEN / "golden.npz")
+
+
+@pytest.fixture(scope="session")
+def golden_meta():
+    with open(GOLDEN / "golden.json") as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def oracle():
+    from oracle import meshdist_oracle
+
+    return meshdist_oracle
+
+
+@pytest.fixture(scope="session")
+def reference():
+    """The live reference package (build container only)."""
+    if not (REFERENCE_SRC / "meshdist" / "__init__.py").exists():
+        pytest.skip("reference not mounted (expected on the GPU box)")
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "meshdist_ref", REFERENCE_SRC / "meshdist" / "__init__.py",
+        submodule_search_locations=[str(REFERENCE_SRC / "meshdist")])
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules["meshdist_ref"] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+@pytest.fixture(scope="session")
+def md():
+    import paper_2411_11244_b200 as md
+
+    return md
+
+
+@pytest.fixture(scope="session")
+def gpu(md):
+    """Skip-free on the GPU box: a gpu test that cannot reach the device fails."""
+    from paper_2411_11244_b200 import _lib
+
+    _lib.require_device()
+    return True

@@ -1,0 +1,271 @@
+"""Parity of the CUDA path with the reference (golden vectors made by the
+reference itself) and with the CPU oracle.  Bar: bitwise for the exact
+kernels, trees and query distances; witness = the brute-force witness
+(lexicographically smallest tied pair)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _eq(a, b, what=""):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (what, a.shape, b.shape)
+    bad = ~((a == b) | (np.isnan(a) & np.isnan(b)))
+    assert not bad.any(), f"{what}: {bad.sum()} mismatches, first {np.argwhere(bad)[:3].tolist()}"
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+@pytest.mark.parametrize("kind", ["min", "max"])
+def test_tri_tri_exact_bitwise(md, gpu, golden, prec, kind):
+    dt = np.float64 if prec == 64 else np.float32
+    t1, t2 = golden["tri_t1"].astype(dt), golden["tri_t2"].astype(dt)
+    d, p, q = (md.batch_tri_tri_min if kind == "min" else md.batch_tri_tri_max)(t1, t2)
+    assert d.dtype == dt
+    _eq(d, golden[f"tri_{kind}{prec}_d"], "d")
+    _eq(p, golden[f"tri_{kind}{prec}_p"], "p")
+    _eq(q, golden[f"tri_{kind}{prec}_q"], "q")
+
+
+@pytest.mark.parametrize("kind", ["min", "max"])
+def test_tri_tri_fast_within_slack(md, gpu, golden, kind):
+    """The traversal's float32 filter stays within E/2 = 2^-16 * max|coord|
+    of the float64 reference distance."""
+    from paper_2411_11244_b200.bounds import tri_tri_fast
+
+    t1, t2 = golden["tri_t1"], golden["tri_t2"]
+    ref = golden[f"tri_{kind}64_d"]
+    fast = tri_tri_fast(kind, t1, t2).astype(np.float64)
+    M = np.maximum(np.abs(t1).reshape(len(t1), -1).max(1), np.abs(t2).reshape(len(t2), -1).max(1))
+    M = np.maximum(M, np.abs(t1.astype(np.float32)).reshape(len(t1), -1).max(1))
+    err = np.abs(fast - ref) / (M * 2.0**-16)
+    assert err.max() <= 1.0, f"max error {err.max():.3g} x (E/2) at {int(err.argmax())}"
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_box_bounds_bitwise(md, gpu, golden, prec):
+    dt = np.float64 if prec == 64 else np.float32
+    bx = [golden[k].astype(dt) for k in ("box_amin", "box_amax", "box_bmin", "box_bmax")]
+    _eq(md.batch_min_lower(*bx), golden[f"box_min_lower{prec}"], "min_lower")
+    _eq(md.batch_max_upper(*bx), golden[f"box_max_upper{prec}"], "max_upper")
+    _eq(md.batch_enhanced_min_upper(*bx), golden[f"box_enh_min_upper{prec}"], "enh_min_upper")
+    _eq(md.batch_enhanced_max_lower(*bx), golden[f"box_enh_max_lower{prec}"], "enh_max_lower")
+
+
+def test_scalar_kat(md, gpu, golden_meta):
+    k = golden_meta["kat"]
+    A = md.Aabb
+    unit = A([0, 0, 0], [1, 1, 1], tight=True)
+    assert md.aabb_min_lower(A([0, 0, 0], [1, 1, 1]), A([2, 0, 0], [3, 1, 1])) == k["min_lower_gap_x"]
+    assert md.aabb_min_lower(A([0, 0, 0], [1, 1, 1]), A([2, 2, 2], [3, 3, 3])) == k["min_lower_diag"]
+    assert md.aabb_max_upper(A([0, 0, 0], [0, 0, 0]), A([1, 1, 1], [2, 2, 2])) == k["max_upper_point"]
+    assert md.enhanced_min_upper(unit, unit) == k["enh_min_upper_unit"]
+    assert md.enhanced_max_lower(unit, unit) == k["enh_max_lower_unit"]
+    with pytest.raises(md.TightnessError):
+        md.enhanced_min_upper(A([0, 0, 0], [1, 1, 1]), unit)
+    d, p, q = md.tri_tri_min([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 0, 1], [1, 0, 1], [0, 1, 1]])
+    assert d == 1.0
+    d, _, _ = md.tri_tri_max([[0, 0, 0], [3, 0, 0], [0, 1, 0]], [[0, 0, 0], [3, 0, 0], [0, 1, 0]])
+    assert d == np.sqrt(10.0)
+
+
+def test_build_trees_bitwise(md, gpu, golden, golden_meta):
+    for name in golden_meta["trees"]:
+        mesh = md.TriangleMesh(golden[f"tree_{name}_V"], golden[f"tree_{name}_T"])
+        for prec, dt in ((64, np.float64), (32, np.float32)):
+            t = md.build_f12(mesh, dtype=dt)
+            _eq(t.prim_order, golden[f"tree_{name}_order"], f"{name} order")
+            _eq(t.leaf_tris, golden[f"tree_{name}_leaf"], f"{name} leaves")
+            assert t.depth == int(golden[f"tree_{name}_depth"])
+            assert t.node_min.dtype == dt
+            _eq(t.node_min, golden[f"tree_{name}_min{prec}"], f"{name} min{prec}")
+            _eq(t.node_max, golden[f"tree_{name}_max{prec}"], f"{name} max{prec}")
+
+
+def test_build_pairing_tori(md, gpu, golden, golden_meta):
+    for rec in golden_meta["pairings"]:
+        tz, _ = md.ring_pair_base(rec["nu"], rec["nv"])
+        t = md.build_f12(tz)
+        _eq(t.leaf_tris.astype(np.int32), golden[f"pair_{rec['name']}_leaf"], rec["name"])
+        _eq(t.prim_order.astype(np.int32), golden[f"pair_{rec['name']}_order"], rec["name"])
+
+
+def test_build_structure_suite(md, gpu, oracle):
+    """SPEC acceptance 7: fullness, 1-2 triangle leaves, tight containment,
+    build -> refit fixed point, at sizes 1, 2, 3, 4, 5, 7, 1000."""
+    for n in (1, 2, 3, 4, 5, 7, 1000):
+        a, _ = md.gen_scene("random-blobs", {"n": n, "seed": 3})
+        t = md.build_f12(a)
+        L = t.leaf_count
+        assert L & (L - 1) == 0 and L <= n < 2 * L and t.n_nodes == 2 * L - 1
+        ids = t.leaf_tris[t.leaf_tris >= 0]
+        assert sorted(ids.tolist()) == list(range(n))
+        before = (t.node_min.copy(), t.node_max.copy())
+        md.refit(t, a)
+        _eq(t.node_min, before[0])
+        _eq(t.node_max, before[1])
+        P = a.triangle_points()
+        for node in range(t.n_nodes):
+            lo_d = t.depth - md.remaining_depth(t, node)
+            first = ((node + 1) << (t.depth - lo_d)) - 1 - (L - 1)
+            ranks = range(first, first + (1 << (t.depth - lo_d)))
+            tris = [x for r in ranks for x in t.leaf_prims(r)]
+            pts = P[tris].reshape(-1, 3)
+            assert np.array_equal(pts.min(0), t.node_min[node]) and np.array_equal(pts.max(0), t.node_max[node])
+
+
+def test_refit_moved_mesh(md, gpu):
+    a, _ = md.gen_scene("interlocked-rings", {"nu": 60, "nv": 30})
+    t = md.build_f12(a)
+    xf = md.RigidTransform.from_axis_angle((0.3, -1, 2), 1.3, (0.5, -0.25, 2.0))
+    moved = md.apply_transform(a, xf)
+    md.refit(t, moved)
+    ref = md.build_f12(md.TriangleMesh(moved.vertices, moved.triangles))
+    # device transform vs numpy dgemm differ by <= 1 ulp per coordinate
+    assert np.allclose(t.node_min, ref.node_min, rtol=0, atol=4e-15 * np.abs(ref.node_min).max())
+    assert np.allclose(t.node_max, ref.node_max, rtol=0, atol=4e-15 * np.abs(ref.node_max).max())
+    with pytest.raises(md.TopologyMismatchError):
+        md.refit(t, md.gen_scene("random-blobs", {"n": 7})[0])
+    # translation commutes with min/max (SPEC refit example)
+    t2 = md.build_f12(a)
+    md.refit(t2, md.apply_transform(a, md.RigidTransform(np.eye(3), (1.0, 2.0, 3.0))))
+    assert np.allclose(t2.node_min, md.build_f12(a).node_min + [1.0, 2.0, 3.0], atol=1e-12)
+
+
+def _check_query(md, ma, mb, prec, rec_q, tag):
+    dt = np.float64 if prec == 64 else np.float32
+    ta, tb = md.build_f12(ma, dtype=dt), md.build_f12(mb, dtype=dt)
+    cfg = md.EngineConfig(precision=prec)
+    for q in ("min", "max"):
+        g = rec_q(q)
+        r = (md.run_min_query if q == "min" else md.run_max_query)(ma, mb, ta, tb, cfg)
+        assert r.distance == g["distance"], (tag, q, prec, r.distance, g["distance"])
+        assert r.distance == g["brute_distance"]
+        assert (r.witness.tri_a, r.witness.tri_b) == (g["brute_tri_a"], g["brute_tri_b"]), (tag, q, prec)
+        assert r.witness_exact
+        if (r.witness.tri_a, r.witness.tri_b) == (g["tri_a"], g["tri_b"]):
+            assert r.witness.point_a.tolist() == g["point_a"] and r.witness.point_b.tolist() == g["point_b"]
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_engine_battery(md, gpu, golden_meta, prec):
+    for rec in golden_meta["engine"]:
+        ma, mb = md.gen_scene(rec["kind"], rec["params"])
+        _check_query(md, ma, mb, prec, lambda q: rec[f"{q}{prec}"], (rec["kind"], rec["params"]))
+
+
+def test_config1_tori_golden(md, gpu, golden_meta):
+    g = golden_meta["config1"]
+    a, b = md.gen_scene("interlocked-rings", {"nu": 100, "nv": 50})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    for q in ("min", "max"):
+        r = (md.run_min_query if q == "min" else md.run_max_query)(a, b, ta, tb)
+        assert r.distance == g[q]["distance"]
+        assert (r.witness.tri_a, r.witness.tri_b) == (g[q]["tri_a"], g[q]["tri_b"])
+        assert r.witness.point_a.tolist() == g[q]["point_a"]
+        assert r.witness.point_b.tolist() == g[q]["point_b"]
+    d, pair = md.min_distance(a, b)
+    assert d == g["min"]["distance"] and pair == (g["min"]["tri_a"], g["min"]["tri_b"])
+    d, pair = md.max_distance(a, b)
+    assert d == g["max"]["distance"] and pair == (g["max"]["tri_a"], g["max"]["tri_b"])
+
+
+def test_rotation_frames_golden(md, gpu, golden_meta):
+    """Config-3 frames through the lazy device transform + refit: distances
+    within 1e-12 relative of the reference (its vertices come from numpy's
+    dgemm, ours from the device formula), identical witnesses."""
+    tz, tb = md.ring_pair_base(100, 50)
+    bvh_a, bvh_b = md.build_f12(tz), md.build_f12(tb)
+    for rec in golden_meta["frames"]:
+        xa, xb = md.ring_frame_transforms(rec["frame"])
+        a, b = md.apply_transform(tz, xa), md.apply_transform(tb, xb)
+        md.refit(bvh_a, a)
+        md.refit(bvh_b, b)
+        for q in ("min", "max"):
+            r = (md.run_min_query if q == "min" else md.run_max_query)(a, b, bvh_a, bvh_b)
+            assert abs(r.distance - rec[q]["distance"]) <= 1e-12 * rec[q]["distance"], (rec["frame"], q)
+            assert (r.witness.tri_a, r.witness.tri_b) == (rec[q]["tri_a"], rec[q]["tri_b"])
+        d, pair = md.min_distance(tz, b, xa)
+        assert abs(d - rec["min"]["distance"]) <= 1e-12 * d and pair == (rec["min"]["tri_a"], rec["min"]["tri_b"])
+
+
+def test_brute_force_device(md, gpu, golden_meta):
+    for rec in golden_meta["engine"][:10]:
+        ma, mb = md.gen_scene(rec["kind"], rec["params"])
+        for prec, dt in ((64, np.float64), (32, np.float32)):
+            for q in ("min", "max"):
+                g = rec[f"{q}{prec}"]
+                d, w = (md.brute_force_min if q == "min" else md.brute_force_max)(ma, mb, dtype=dt)
+                assert (d, w.tri_a, w.tri_b) == (g["brute_distance"], g["brute_tri_a"], g["brute_tri_b"])
+    a, b = md.gen_scene("random-blobs", {"n": 4000})
+    with pytest.raises(md.SizeGuardError):
+        md.brute_force_min(a, b)
+
+
+def test_variants_agree(md, gpu):
+    """SPEC acceptance 5/9 analogues: culling off, enhanced bounds off, k = 1,
+    warm start and guarantee_witness all give the same distance + witness."""
+    for kind, params in [("random-blobs", {"n": 300, "seed": 4}), ("offset-grids", {"res": 14}),
+                         ("nested-shells", {"lat": 12, "lon": 16, "r_outer": 0.85}),
+                         ("intersecting-clusters", {"n": 400, "seed": 9})]:
+        a, b = md.gen_scene(kind, params)
+        ta, tb = md.build_f12(a), md.build_f12(b)
+        for q in ("min", "max"):
+            run = md.run_min_query if q == "min" else md.run_max_query
+            base = run(a, b, ta, tb)
+            for cfg in (md.EngineConfig(culling=False, front_hard_cap=1 << 26), md.EngineConfig(enhanced_bounds=False),
+                        md.EngineConfig(depth_cap=1), md.EngineConfig(guarantee_witness=True)):
+                r = run(a, b, ta, tb, cfg)
+                assert r.distance == base.distance and (r.witness.tri_a, r.witness.tri_b) == (
+                    base.witness.tri_a, base.witness.tri_b), (kind, q, cfg)
+            warm = run(a, b, ta, tb, warm_pair=(base.witness.tri_a, base.witness.tri_b))
+            assert warm.distance == base.distance
+            assert warm.expanded_pairs <= base.expanded_pairs
+        if kind == "intersecting-clusters":
+            assert base.distance == 0.0 or q == "max"
+
+
+def test_degenerate_depths(md, gpu, oracle):
+    """depth-0 trees and mixed depths (query.py:368-377, 510-518)."""
+    a1 = md.TriangleMesh([[0, 0, 0.0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]])
+    a3, _ = md.gen_scene("random-blobs", {"n": 3, "seed": 1})
+    big, _ = md.gen_scene("interlocked-rings", {"nu": 60, "nv": 40})
+    for ma, mb in ((a1, a1), (a1, big), (big, a1), (a3, big), (big, a3)):
+        ta, tb = md.build_f12(ma), md.build_f12(mb)
+        for q in ("min", "max"):
+            r = (md.run_min_query if q == "min" else md.run_max_query)(ma, mb, ta, tb)
+            d, ia, ib, _, _ = oracle.brute_force(ma.triangle_points(), mb.triangle_points(), q, force=True)
+            assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (ia, ib)
+
+
+def test_errors(md, gpu):
+    a, b = md.gen_scene("nested-shells", {"lat": 40, "lon": 40, "r_outer": 0.82})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    with pytest.raises(md.FrontOverflowError) as ei:
+        md.run_max_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=64))
+    assert ei.value.cap == 64 and ei.value.candidates > 64
+    with pytest.raises(md.ConfigError):
+        md.run_min_query(a, b, ta, tb, md.EngineConfig(precision=32))
+    # the workspace is healthy after an overflow
+    assert md.run_min_query(a, b, ta, tb).distance > 0
+
+
+def test_expand_front_step_api(md, gpu, oracle):
+    """The single-step API reproduces the reference loop bit for bit."""
+    a, b = md.gen_scene("random-blobs", {"n": 200, "seed": 2})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    cfg = md.EngineConfig()
+    pa, pb = a.triangle_points(), b.triangle_points()
+    r = md.batch_min_lower(ta.node_min[:1], ta.node_max[:1], tb.node_min[:1], tb.node_max[:1])[0]
+    st = md.QueryState("min", md.batch_enhanced_min_upper(ta.node_min[:1], ta.node_max[:1], tb.node_min[:1],
+                                                          tb.node_max[:1])[0])
+    front = md.Front(np.zeros(1, np.int64), np.zeros(1, np.int64), np.asarray([r]), 0, 0)
+    while len(front):
+        k = md.adaptive_depth(len(front), cfg, max(ta.depth - front.depth_a, tb.depth - front.depth_b))
+        front = md.expand_front(front, k, st, ta, tb, pa, pb, cfg)
+    want = oracle.run_query(oracle.build_tree(a.vertices, a.triangles), oracle.build_tree(b.vertices, b.triangles),
+                            pa, pb, "min")
+    assert st.bound == want.distance
+    assert [(s.k, s.front_in, s.front_out, s.culled, s.bound_after) for s in st.iterations] == [
+        tuple(x) for x in want.iterations]
