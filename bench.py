@@ -209,7 +209,10 @@ def run_ours(args):
     results = []
     for i in range(W, W + K):
         a, b, pq = prepared[i]
-        pq.launch()  # re-run to read back stats (the timed launches share one workspace)
+        # re-run to read back stats (the timed launches share one workspace)
+        bvh_a._device_refit(a)
+        bvh_b._device_refit(b)
+        pq.launch()
         results.append(pq.collect())
     if dist:
         t = torch.tensor([region_ms], device=dev)
@@ -333,7 +336,9 @@ def cpu_frame_query(oracle, ta, tb, tz, tbm, f, kind, workers):
     oracle.fill_boxes(tb, vb, tbm.triangles)
     pa = oracle.triangle_points(va, tz.triangles)
     pb = oracle.triangle_points(vb, tbm.triangles)
-    return oracle.run_query(ta, tb, pa, pb, kind, oracle.Config(workers=workers))
+    # front_hard_cap raised like the GPU run's: at the default 2^24 the
+    # reference raises FrontOverflowError on this workload (query.py:375)
+    return oracle.run_query(ta, tb, pa, pb, kind, oracle.Config(workers=workers, front_hard_cap=1 << 27))
 
 
 def cpu_baseline(args, ctx, budget):

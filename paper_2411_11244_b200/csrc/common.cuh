@@ -64,7 +64,11 @@ template <typename T> struct Fast {
   static __device__ __forceinline__ T add(T a, T b) { return a + b; }
   static __device__ __forceinline__ T sub(T a, T b) { return a - b; }
   static __device__ __forceinline__ T mul(T a, T b) { return a * b; }
-  static __device__ __forceinline__ T div(T a, T b) { return a / b; }
+  // approximate division (MUFU.RCP based): the float32 filter's error budget
+  // absorbs its 2-ulp error on clamped parameters
+  static __device__ __forceinline__ T div(T a, T b) { return fast_div(a, b); }
+  static __device__ __forceinline__ float fast_div(float a, float b) { return __fdividef(a, b); }
+  static __device__ __forceinline__ double fast_div(double a, double b) { return a / b; }
   static __device__ __forceinline__ T sqrt(T a) { return ::sqrt(a); }
 };
 

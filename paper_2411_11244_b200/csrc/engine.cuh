@@ -22,8 +22,12 @@ struct alignas(16) QState {
   long long ov_cand, ov_in, ov_cap;
   float slack;
   int band_overflow;
+  unsigned n_seed;                   // blocks that wrote a seed leaf pair
+  int _pad2;
   GdIterStat stats[kMaxIters];
 };
+
+constexpr int kMaxSeeds = 8192;
 
 struct QArgs {
   GdMesh ma, mb;
@@ -34,6 +38,8 @@ struct QArgs {
   float* key[2];
   uint2* band_ids;
   float* band_d;
+  uint2* seed_pair;             // per expand block: its best leaf pair
+  float* seed_key;
   unsigned long long cap;       // front / leaf-list capacity (entries)
   unsigned long long band_cap;  // band capacity (entries)
   GdResult* result;             // device result record
@@ -73,6 +79,17 @@ __device__ __forceinline__ Tri<float> load_tri32(const GdBvh& T, const int4& s) 
   t.v[1] = {b.x, b.y, b.z};
   t.v[2] = {c.x, c.y, c.z};
   return t;
+}
+
+__device__ __forceinline__ Box tri_box(const Tri<float>& t) {
+  Box b;
+  b.lo[0] = fminf(fminf(t.v[0].x, t.v[1].x), t.v[2].x);
+  b.lo[1] = fminf(fminf(t.v[0].y, t.v[1].y), t.v[2].y);
+  b.lo[2] = fminf(fminf(t.v[0].z, t.v[1].z), t.v[2].z);
+  b.hi[0] = fmaxf(fmaxf(t.v[0].x, t.v[1].x), t.v[2].x);
+  b.hi[1] = fmaxf(fmaxf(t.v[0].y, t.v[1].y), t.v[2].y);
+  b.hi[2] = fmaxf(fmaxf(t.v[0].z, t.v[1].z), t.v[2].z);
+  return b;
 }
 
 // float64 vertex of a mesh with its rigid transform applied (mesh.py:102-105)

@@ -174,28 +174,28 @@ struct Box {
   float lo[3], hi[3];
 };
 
-__device__ __forceinline__ float box_min_lower(const Box& a, const Box& b) {
+__device__ __forceinline__ float box_min_lower_sq(const Box& a, const Box& b) {
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     float g = fmaxf(fmaxf(a.lo[k] - b.hi[k], b.lo[k] - a.hi[k]), 0.f);
     s = fmaf(g, g, s);
   }
-  return sqrtf(s);
+  return s;
 }
 
-__device__ __forceinline__ float box_max_upper(const Box& a, const Box& b) {
+__device__ __forceinline__ float box_max_upper_sq(const Box& a, const Box& b) {
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     float h = fmaxf(fabsf(a.lo[k] - b.hi[k]), fabsf(a.hi[k] - b.lo[k]));
     s = fmaf(h, h, s);
   }
-  return sqrtf(s);
+  return s;
 }
 
 // Eq. 9: min over face pairs of the face-rectangle max distance.
-__device__ __forceinline__ float box_enhanced_min_upper(const Box& a, const Box& b) {
+__device__ __forceinline__ float box_enhanced_min_upper_sq(const Box& a, const Box& b) {
   float H2[3], PA2[3], PB2[3], PP2[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -219,11 +219,11 @@ __device__ __forceinline__ float box_enhanced_min_upper(const Box& a, const Box&
   best = fminf(best, H2[0] + PA2[1] + PB2[2]);
   best = fminf(best, PB2[0] + H2[1] + PA2[2]);
   best = fminf(best, H2[0] + PB2[1] + PA2[2]);
-  return sqrtf(best);
+  return best;
 }
 
 // Eq. 10: max over face pairs of the face-rectangle min distance.
-__device__ __forceinline__ float box_enhanced_max_lower(const Box& a, const Box& b) {
+__device__ __forceinline__ float box_enhanced_max_lower_sq(const Box& a, const Box& b) {
   float G2[3], QA2[3], QB2[3], QQ2[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -246,7 +246,10 @@ __device__ __forceinline__ float box_enhanced_max_lower(const Box& a, const Box&
   best = fmaxf(best, G2[0] + QA2[1] + QB2[2]);
   best = fmaxf(best, QB2[0] + G2[1] + QA2[2]);
   best = fmaxf(best, G2[0] + QB2[1] + QA2[2]);
-  return sqrtf(best);
+  return best;
 }
+
+__device__ __forceinline__ float box_min_lower(const Box& a, const Box& b) { return sqrtf(box_min_lower_sq(a, b)); }
+__device__ __forceinline__ float box_max_upper(const Box& a, const Box& b) { return sqrtf(box_max_upper_sq(a, b)); }
 
 }  // namespace gd

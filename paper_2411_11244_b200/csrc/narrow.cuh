@@ -1,0 +1,332 @@
+// narrow.cuh -- narrow phase (query.py:287-346, bounds.py:245-330):
+// float32 filter over the leaf-pair list, exact pass over the band, and the
+// witness record.
+#pragma once
+
+#include "traverse.cuh"
+
+namespace gd {
+
+constexpr int kNarrowThreads = 256;
+
+// exact narrow phase for one triangle pair -> 128-bit key (distance bits,
+// tri_a, tri_b): its minimum is the reference's lexicographic witness rule
+// (query.py:205-220, 299)
+template <bool kMax>
+__device__ __forceinline__ Key128 exact_key(const QArgs& q, unsigned ta, unsigned tb) {
+  double d;
+  if (q.cfg.precision == 32) {
+    Tri<float> a = mesh_tri<float>(q.ma, ta), b = mesh_tri<float>(q.mb, tb);
+    float d2 = kMax ? tri_tri_max_d2<Exact<float>, float, false>(a, b, nullptr, nullptr)
+                    : tri_tri_min_d2<Exact<float>, float, false>(a, b, nullptr, nullptr);
+    d = (double)__fsqrt_rn(d2);
+  } else {
+    Tri<double> a = mesh_tri<double>(q.ma, ta), b = mesh_tri<double>(q.mb, tb);
+    double d2 = kMax ? tri_tri_max_d2<Exact<double>, double, false>(a, b, nullptr, nullptr)
+                     : tri_tri_min_d2<Exact<double>, double, false>(a, b, nullptr, nullptr);
+    d = __dsqrt_rn(d2);
+  }
+  unsigned long long bits = (unsigned long long)__double_as_longlong(d);
+  Key128 k;
+  k.hi = kMax ? ~bits : bits;  // d >= 0: bit order == value order
+  k.lo = ((unsigned long long)ta << 32) | tb;
+  return k;
+}
+
+__device__ __forceinline__ Key128 shfl_key(Key128 k, int o) {
+  Key128 r;
+  r.hi = __shfl_xor_sync(0xffffffffu, k.hi, o);
+  r.lo = __shfl_xor_sync(0xffffffffu, k.lo, o);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// fast float32 narrow phase over the leaf-pair list: every leaf pair expands
+// to its 1..4 triangle pairs inside the block (block scan), a triangle-box
+// prefilter compacts the survivors, then the full test runs on dense lanes.
+template <bool kMax, bool kRescan>
+__global__ __launch_bounds__(kNarrowThreads) void k_narrow(QArgs q) {
+  QState* S = q.S;
+  const unsigned long long n = S->n_leaf;
+  if (n == 0) return;
+  // rescan pass: only when the band overflowed; re-filters every pair with
+  // the final bound and evaluates the survivors exactly
+  if (kRescan && *reinterpret_cast<volatile int*>(&S->band_overflow) == 0) return;
+  if (blockIdx.x * (unsigned long long)kNarrowThreads >= n) return;
+  __shared__ unsigned warp_tot[kNarrowThreads / 32];
+  __shared__ unsigned char owner[kNarrowThreads * 4];
+  __shared__ unsigned s_off[kNarrowThreads];
+  __shared__ uint2 s_first[kNarrowThreads];
+  __shared__ unsigned char s_cb[kNarrowThreads];
+  __shared__ float warp_upd[kNarrowThreads / 32];
+  __shared__ unsigned short work[kNarrowThreads * 4];
+  __shared__ unsigned n_work;
+  const int buf = S->leaf_buf;
+  const uint2* __restrict__ leaves = q.node[buf];
+  const float* __restrict__ keys = q.key[buf];
+  const float E = S->slack;
+  const bool culling = q.cfg.culling != 0;
+  unsigned long long my_pairs = 0;
+  const int4* __restrict__ lta = reinterpret_cast<const int4*>(q.A.leaf_tri);
+  const int4* __restrict__ ltb = reinterpret_cast<const int4*>(q.B.leaf_tri);
+
+  for (unsigned long long tile = blockIdx.x; tile * kNarrowThreads < n; tile += gridDim.x) {
+    const unsigned long long i = tile * kNarrowThreads + threadIdx.x;
+    const float ub = load_bound(S);
+    unsigned cnt = 0;
+    uint2 first = make_uint2(0, 0);
+    unsigned cb = 1;
+    if (i < n) {
+      const float pk = keys[i];  // squared leaf-pair key
+      if (!culling || survives<kMax>(pk, ub * ub)) {
+        const uint2 lp = leaves[i];
+        const unsigned fa = __ldg(q.A.leaf_first + lp.x), ca = __ldg(q.A.leaf_first + lp.x + 1) - fa;
+        const unsigned fb = __ldg(q.B.leaf_first + lp.y);
+        cb = __ldg(q.B.leaf_first + lp.y + 1) - fb;
+        first = make_uint2(fa, fb);
+        cnt = ca * cb;
+      }
+    }
+    unsigned total;
+    const unsigned off = block_exclusive_scan(cnt, warp_tot, total);
+    s_off[threadIdx.x] = off;
+    s_first[threadIdx.x] = first;
+    s_cb[threadIdx.x] = (unsigned char)cb;
+    for (unsigned j = 0; j < cnt; ++j) owner[off + j] = (unsigned char)threadIdx.x;
+    if (threadIdx.x == 0) n_work = 0;
+    __syncthreads();
+    // stage 1: triangle-box prefilter, survivors compacted into `work`
+    const float ub1 = load_bound_sq(S);
+    for (unsigned s = threadIdx.x; s < total; s += kNarrowThreads) {
+      const int o = owner[s];
+      const unsigned j = s - s_off[o];
+      const unsigned cbo = s_cb[o];
+      const uint2 f = s_first[o];
+      const int4 sa = __ldg(lta + f.x + j / cbo);
+      const int4 sb = __ldg(ltb + f.y + j % cbo);
+      const Box ba = tri_box(load_tri32(q.A, sa)), bb = tri_box(load_tri32(q.B, sb));
+      if (!culling || survives<kMax>(pair_key<kMax>(ba, bb), ub1)) work[atomicAdd(&n_work, 1u)] = (unsigned short)s;
+    }
+    __syncthreads();
+    const unsigned nw = n_work;
+    float upd = kMax ? 0.f : INFINITY;
+    // stage 2: full narrow phase on the compacted survivors
+    for (unsigned w = threadIdx.x; w < nw; w += kNarrowThreads) {
+      const unsigned s = work[w];
+      const int o = owner[s];
+      const unsigned j = s - s_off[o];
+      const unsigned cbo = s_cb[o];
+      const uint2 f = s_first[o];
+      const int4 sa = __ldg(lta + f.x + j / cbo);
+      const int4 sb = __ldg(ltb + f.y + j % cbo);
+      const Tri<float> A = load_tri32(q.A, sa), B = load_tri32(q.B, sb);
+      const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
+                           : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+      upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
+      const bool cand = kMax ? (d + E >= ub) : (d - E <= ub);
+      if (cand) {
+        if (kRescan) {
+          atomic_min_key(&S->best, exact_key<kMax>(q, (unsigned)sa.w, (unsigned)sb.w));
+          atomicAdd(&S->band_eval, 1ull);
+        } else {
+          const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
+          if (slot < q.band_cap) {
+            q.band_ids[slot] = make_uint2((unsigned)sa.w, (unsigned)sb.w);
+            q.band_d[slot] = d;
+          } else {
+            S->band_overflow = 1;  // k_narrow<kMax, true> re-scans the leaf list
+          }
+        }
+      }
+    }
+    if (kRescan) {
+      __syncthreads();
+      continue;
+    }
+    my_pairs += nw;
+    upd = kMax ? warp_max(upd) : warp_min(upd);
+    if ((threadIdx.x & 31) == 0) warp_upd[threadIdx.x >> 5] = upd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float u = warp_upd[0];
+      for (int w = 1; w < kNarrowThreads / 32; ++w) u = kMax ? fmaxf(u, warp_upd[w]) : fminf(u, warp_upd[w]);
+      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, u);
+    }
+    __syncthreads();
+  }
+  if (!kRescan && threadIdx.x == 0 && my_pairs) atomicAdd(&S->narrow, my_pairs);
+}
+
+// ---------------------------------------------------------------------------
+// exact pass over the band: only pairs whose float32 distance can still be
+// the answer (|d_fast - d_exact| <= E/2) are re-evaluated in the reference's
+// arithmetic; the 128-bit minimum is the answer and its witness.
+template <bool kMax>
+__global__ __launch_bounds__(256) void k_refine(QArgs q) {
+  QState* S = q.S;
+  const unsigned long long n = min(S->n_band, q.band_cap);
+  if (blockIdx.x * 256ull >= n) return;
+  const float E = S->slack;
+  const float ub = load_bound(S);
+  __shared__ Key128 wk[8];
+  Key128 best;
+  best.hi = ~0ull;
+  best.lo = ~0ull;
+  unsigned long long evals = 0;
+  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
+    const float d = q.band_d[i];
+    if (kMax ? (d + E >= ub) : (d - E <= ub)) {
+      const uint2 ids = q.band_ids[i];
+      Key128 k = exact_key<kMax>(q, ids.x, ids.y);
+      if (key_less(k, best)) best = k;
+      ++evals;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Key128 other = shfl_key(best, o);
+    if (key_less(other, best)) best = other;
+  }
+  evals = warp_sum_u64(evals);
+  if ((threadIdx.x & 31) == 0) {
+    wk[threadIdx.x >> 5] = best;
+    if (evals) atomicAdd(&S->band_eval, evals);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (key_less(wk[w], best)) best = wk[w];
+    if (best.hi != ~0ull) atomic_min_key(&S->best, best);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Witness points of one triangle pair, one warp: lane l evaluates feature l
+// of the reference's fixed order (9 edge pairs, then A_i->B / B_i->A), the
+// warp keeps the first strict optimum, then the 6 pierce tests run in lanes
+// 0..5 and the first hit wins -- the sequential semantics of
+// bounds.py:245-330 at 1/15 of its latency.
+template <typename T>
+__device__ __forceinline__ void shfl_v3(V3<T>& v, int src) {
+  v.x = __shfl_sync(0xffffffffu, v.x, src);
+  v.y = __shfl_sync(0xffffffffu, v.y, src);
+  v.z = __shfl_sync(0xffffffffu, v.z, src);
+}
+
+template <typename T, bool kMax>
+__device__ void warp_witness(const Tri<T>& a, const Tri<T>& b, V3<T>& P, V3<T>& Q) {
+  using A = Exact<T>;
+  const int lane = threadIdx.x & 31;
+  T d2 = kMax ? T(-1) : T(INFINITY);
+  V3<T> p{T(0), T(0), T(0)}, qq{T(0), T(0), T(0)};
+  if (kMax) {
+    if (lane < 9) {
+      p = a.v[lane / 3];
+      qq = b.v[lane % 3];
+      V3<T> w = vsub<A>(p, qq);
+      d2 = vdot<A>(w, w);
+    }
+  } else if (lane < 9) {
+    const int i = lane / 3, j = lane % 3;
+    segment_pair<A>(a.v[i], vsub<A>(a.v[(i + 1) % 3], a.v[i]), b.v[j], vsub<A>(b.v[(j + 1) % 3], b.v[j]), p, qq);
+    V3<T> w = vsub<A>(p, qq);
+    d2 = vdot<A>(w, w);
+  } else if (lane < 15) {
+    const int i = (lane - 9) >> 1;
+    if (((lane - 9) & 1) == 0) {
+      p = a.v[i];
+      qq = point_triangle<A>(a.v[i], b.v[0], b.v[1], b.v[2]);
+    } else {
+      qq = b.v[i];
+      p = point_triangle<A>(b.v[i], a.v[0], a.v[1], a.v[2]);
+    }
+    V3<T> w = vsub<A>(p, qq);
+    d2 = vdot<A>(w, w);
+  }
+  // first strict optimum in feature order == (d2, lane) lexicographic
+  T bd = d2;
+  int bl = lane;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const T od = __shfl_xor_sync(0xffffffffu, bd, o);
+    const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+    if ((kMax ? od > bd : od < bd) || (od == bd && ol < bl)) {
+      bd = od;
+      bl = ol;
+    }
+  }
+  shfl_v3(p, bl);
+  shfl_v3(qq, bl);
+  if (!kMax && bd > T(0)) {
+    bool hit = false;
+    V3<T> x{T(0), T(0), T(0)};
+    if (lane < 6) {
+      const int i = lane >> 1;
+      hit = (lane & 1) == 0 ? pierce<A>(a.v[i], a.v[(i + 1) % 3], b.v[0], b.v[1], b.v[2], x)
+                            : pierce<A>(b.v[i], b.v[(i + 1) % 3], a.v[0], a.v[1], a.v[2], x);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) {
+      const int src = __ffs(m) - 1;
+      shfl_v3(x, src);
+      p = x;
+      qq = x;
+    }
+  }
+  P = p;
+  Q = qq;
+}
+
+template <bool kMax>
+__global__ void k_final(QArgs q) {
+  QState* S = q.S;
+  const Key128 best = S->best;
+  const bool found = !(best.hi == ~0ull && best.lo == ~0ull);
+  const unsigned ta = (unsigned)(best.lo >> 32), tb = (unsigned)(best.lo & 0xffffffffu);
+  double pa[3] = {0, 0, 0}, pb[3] = {0, 0, 0};
+  if (found) {
+    if (q.cfg.precision == 32) {
+      Tri<float> a = mesh_tri<float>(q.ma, ta), b = mesh_tri<float>(q.mb, tb);
+      V3<float> p, qq;
+      warp_witness<float, kMax>(a, b, p, qq);
+      pa[0] = p.x; pa[1] = p.y; pa[2] = p.z;
+      pb[0] = qq.x; pb[1] = qq.y; pb[2] = qq.z;
+    } else {
+      Tri<double> a = mesh_tri<double>(q.ma, ta), b = mesh_tri<double>(q.mb, tb);
+      V3<double> p, qq;
+      warp_witness<double, kMax>(a, b, p, qq);
+      pa[0] = p.x; pa[1] = p.y; pa[2] = p.z;
+      pb[0] = qq.x; pb[1] = qq.y; pb[2] = qq.z;
+    }
+  }
+  if (threadIdx.x != 0) return;
+  GdResult r;
+  memset(&r, 0, sizeof(r));
+  r.status = S->err;
+  r.iterations = min(S->iter, kMaxIters);
+  r.expanded_pairs = (long long)S->expanded;
+  r.narrow_pairs = (long long)S->narrow;
+  r.band_pairs = (long long)S->band_eval;
+  r.overflow_candidates = S->ov_cand;
+  r.overflow_front_in = S->ov_in;
+  r.overflow_cap = S->ov_cap;
+  if (!found) {
+    r.tri_a = r.tri_b = -1;
+    const float b = load_bound(S);
+    r.distance = kMax ? (double)b + (double)S->slack : (double)b - (double)S->slack;
+    r.witness_distance = r.distance;
+  } else {
+    const unsigned long long bits = kMax ? ~best.hi : best.hi;
+    r.distance = __longlong_as_double((long long)bits);
+    r.witness_distance = r.distance;
+    r.tri_a = ta;
+    r.tri_b = tb;
+    for (int c = 0; c < 3; ++c) {
+      r.point_a[c] = pa[c];
+      r.point_b[c] = pb[c];
+    }
+  }
+  *q.result = r;
+}
+
+}  // namespace gd

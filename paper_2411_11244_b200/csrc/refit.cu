@@ -23,17 +23,7 @@ __global__ __launch_bounds__(256) void k_xform(GdMesh m, float4* __restrict__ ou
   out[i] = make_float4((float)v.x, (float)v.y, (float)v.z, 0.f);
 }
 
-__device__ __forceinline__ Box tri_box32(const GdBvh& T, const int4& s) {
-  Tri<float> t = load_tri32(T, s);
-  Box b;
-  b.lo[0] = fminf(fminf(t.v[0].x, t.v[1].x), t.v[2].x);
-  b.lo[1] = fminf(fminf(t.v[0].y, t.v[1].y), t.v[2].y);
-  b.lo[2] = fminf(fminf(t.v[0].z, t.v[1].z), t.v[2].z);
-  b.hi[0] = fmaxf(fmaxf(t.v[0].x, t.v[1].x), t.v[2].x);
-  b.hi[1] = fmaxf(fmaxf(t.v[0].y, t.v[1].y), t.v[2].y);
-  b.hi[2] = fmaxf(fmaxf(t.v[0].z, t.v[1].z), t.v[2].z);
-  return b;
-}
+__device__ __forceinline__ Box tri_box32(const GdBvh& T, const int4& s) { return tri_box(load_tri32(T, s)); }
 
 // fold `levels` levels inside the block; sb holds blockDim.x boxes of level
 // `lv`, the block covering nodes [first_rank, first_rank + blockDim.x)

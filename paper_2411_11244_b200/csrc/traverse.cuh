@@ -1,0 +1,516 @@
+// traverse.cuh -- root setup and BVTT front expansion (query.py:266-509).
+#pragma once
+
+#include "engine.cuh"
+
+namespace gd {
+
+constexpr int kExpandThreads = 256;
+constexpr int kGenericItems = 4;                                   // candidates / thread (k >= 2)
+constexpr int kGenericTile = kExpandThreads * kGenericItems;
+constexpr int kK1Rounds = 4;                                       // entries / thread / tile (k == 1)
+constexpr int kK1Tile = kExpandThreads * kK1Rounds;
+constexpr int kK1Stage = kK1Tile * 4;                              // staged survivors (<= 4 / entry)
+constexpr size_t kExpandDynSmem = kK1Stage * (sizeof(uint2) + sizeof(float));
+
+__device__ __forceinline__ float load_bound(const QState* S) {
+  return __uint_as_float(*reinterpret_cast<const volatile unsigned int*>(&S->bound_bits));
+}
+
+template <bool kMax>
+__device__ __forceinline__ bool improves(float a, float b) {
+  return kMax ? a > b : a < b;
+}
+
+// a candidate survives while its key can still beat the (slack-carrying) bound
+template <bool kMax>
+__device__ __forceinline__ bool survives(float key, float bound) {
+  return kMax ? key >= bound : key <= bound;
+}
+
+template <bool kMax>
+__device__ __forceinline__ void commit_bound(QState* S, float v) {
+  if (kMax)
+    atomic_max_pos(&S->bound_bits, v - S->slack);
+  else
+    atomic_min_pos(&S->bound_bits, v + S->slack);
+}
+
+// Keys and bound updates are kept SQUARED inside the traversal (no sqrt per
+// candidate); the bound cell itself is a distance, squared once per tile.
+// key of a node pair: box min distance^2 (min query) / box max distance^2 (max)
+template <bool kMax>
+__device__ __forceinline__ float pair_key(const Box& a, const Box& b) {
+  return kMax ? box_max_upper_sq(a, b) : box_min_lower_sq(a, b);
+}
+
+// bound contribution^2 of a kept pair (query.py:416-423): the enhanced bound
+// of tight boxes, or the conventional one when enhanced bounds are off
+template <bool kMax>
+__device__ __forceinline__ float pair_update(const Box& a, const Box& b, bool enh) {
+  if (kMax) return enh ? box_enhanced_max_lower_sq(a, b) : box_min_lower_sq(a, b);
+  return enh ? box_enhanced_min_upper_sq(a, b) : box_max_upper_sq(a, b);
+}
+
+__device__ __forceinline__ float load_bound_sq(const QState* S) {
+  const float b = load_bound(S);
+  return b * b;
+}
+
+// block-wide exclusive scan of small counts (blockDim.x == kExpandThreads)
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* warp_tot, unsigned& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  unsigned off = 0, tot = 0;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) {
+    unsigned t = warp_tot[w];
+    if (w < wid) off += t;
+    tot += t;
+  }
+  total = tot;
+  return off + x - v;
+}
+
+// ---------------------------------------------------------------------------
+template <bool kMax>
+__global__ void k_init(QArgs q) {
+  if (threadIdx.x != 0) return;
+  QState* S = q.S;
+  Box ra = load_box(q.A.box, 0), rb = load_box(q.B.box, 0);
+  float M = 0.f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    M = fmaxf(M, fmaxf(fmaxf(fabsf(ra.lo[k]), fabsf(ra.hi[k])), fmaxf(fabsf(rb.lo[k]), fabsf(rb.hi[k]))));
+  // slack: 256 float32 ulps of the largest coordinate
+  const float E = M * 0x1p-15f;
+  S->slack = E;
+  const float key0 = pair_key<kMax>(ra, rb);  // squared
+  const float b0 = sqrtf(pair_update<kMax>(ra, rb, q.cfg.enhanced_bounds != 0));
+  S->bound_bits = __float_as_uint(kMax ? fmaxf(b0 - E, 0.f) : b0 + E);
+  S->best.hi = ~0ull;
+  S->best.lo = ~0ull;
+  S->done = 0;
+  S->err = 0;
+  S->cur = 0;
+  S->depth_a = 0;
+  S->depth_b = 0;
+  S->iter = 0;
+  S->leaf_buf = 1;
+  S->n_out = 0;
+  S->n_leaf = 0;
+  S->n_band = 0;
+  S->expanded = 0;
+  S->narrow = 0;
+  S->culled = 0;
+  S->band_eval = 0;
+  S->band_overflow = 0;
+  S->n_seed = 0;
+  S->ov_cand = S->ov_in = S->ov_cap = 0;
+  q.node[0][0] = make_uint2(0, 0);
+  q.key[0][0] = key0;
+  if (q.A.depth == 0 && q.B.depth == 0) {
+    // both roots are leaves: narrow phase immediately (query.py:510-518)
+    q.node[1][0] = make_uint2(0, 0);
+    q.key[1][0] = key0;
+    S->n_leaf = 1;
+    S->n_in = 0;
+    GdIterStat st;
+    st.k = 0;
+    st.front_in = 1;
+    st.front_out = 0;
+    st.culled = 0;
+    st.bound_after = b0;
+    st._pad = 0;
+    S->stats[0] = st;
+    S->iter = 1;
+  } else {
+    S->n_in = 1;
+  }
+  if (q.cfg.warm_a >= 0) {
+    // warm_pair seeds the bound with one exact pair (query.py:494-502)
+    unsigned ta = (unsigned)q.cfg.warm_a, tb = (unsigned)q.cfg.warm_b;
+    const int32_t* ia = q.ma.tri + 3 * (long long)ta;
+    const int32_t* ib = q.mb.tri + 3 * (long long)tb;
+    Tri<float> a = load_tri32(q.A, make_int4(ia[0], ia[1], ia[2], 0));
+    Tri<float> b = load_tri32(q.B, make_int4(ib[0], ib[1], ib[2], 0));
+    float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(a, b, nullptr, nullptr))
+                   : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(a, b, nullptr, nullptr));
+    commit_bound<kMax>(S, d);
+    q.band_ids[0] = make_uint2(ta, tb);
+    q.band_d[0] = d;
+    S->n_band = 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Shared per-block plumbing of an expansion sweep: survivors are compacted
+// with one block scan + one global atomic per tile, bound updates reduced to
+// one atomic per tile (the paper's block-wise reduction).
+struct ExpandShared {
+  unsigned warp_tot[kExpandThreads / 32];
+  unsigned long long out_base;
+  float warp_upd[kExpandThreads / 32];
+  unsigned long long red_culled[kExpandThreads / 32];
+  uint2 warp_seed[kExpandThreads / 32];
+  unsigned stage_count;
+};
+
+template <bool kMax>
+__device__ __forceinline__ unsigned long long tile_commit(ExpandShared& sh, QState* S, unsigned count, float upd,
+                                                         unsigned& my_off) {
+  unsigned total;
+  my_off = block_exclusive_scan(count, sh.warp_tot, total);
+  upd = kMax ? warp_max(upd) : warp_min(upd);
+  if ((threadIdx.x & 31) == 0) sh.warp_upd[threadIdx.x >> 5] = upd;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sh.out_base = total ? atomicAdd(&S->n_out, (unsigned long long)total) : 0ull;
+    float u = sh.warp_upd[0];
+    for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
+    if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
+  }
+  __syncthreads();
+  return sh.out_base;
+}
+
+// One expansion sweep (query.py:349-451, Alg. 2).  Two mappings, chosen
+// uniformly per launch from the adaptive depth k:
+//  k == 1 (the wide late iterations): one thread per front entry; it loads the
+//          (1 or 2) child boxes of each side once (contiguous siblings) and
+//          tests the <= 4 child pairs -- 14 loads per entry instead of 32.
+//  k >= 2 (narrow early fronts, ncand < front_cap): one thread per candidate,
+//          t -> entry t >> (ka+kb), descendants ((node+1) << k) - 1 + offset.
+// Only blocks that own a tile take part, so a small front costs a few blocks.
+template <bool kMax>
+__global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
+  QState* S = q.S;
+  const unsigned long long n_in = S->n_in;
+  if (n_in == 0) return;
+  __shared__ ExpandShared sh;
+
+  const int ra = q.A.depth - S->depth_a, rb = q.B.depth - S->depth_b;
+  const int rem = max(ra, rb);
+  const int k = adaptive_k(n_in, q.cfg.front_cap, q.cfg.depth_cap, rem);
+  const int ka = min(k, ra), kb = min(k, rb), shift = ka + kb;
+  const bool to_leaves = (k == rem);
+  const unsigned long long ncand = n_in << shift;
+  const bool overflow = ncand > (unsigned long long)q.cfg.front_hard_cap;
+  const bool k1 = (k == 1);
+  const unsigned long long tiles = k1 ? (n_in + kK1Tile - 1) / kK1Tile : (ncand + kGenericTile - 1) / kGenericTile;
+  const unsigned active = overflow ? 1u : (unsigned)min((unsigned long long)gridDim.x, tiles);
+  if (blockIdx.x >= active) return;
+
+  const int cur = S->cur;
+  const uint2* __restrict__ in_node = q.node[cur];
+  const float* __restrict__ in_key = q.key[cur];
+  uint2* out_node = q.node[cur ^ 1];
+  float* out_key = q.key[cur ^ 1];
+  const unsigned leaf_a0 = (unsigned)((1ull << q.A.depth) - 1), leaf_b0 = (unsigned)((1ull << q.B.depth) - 1);
+  const unsigned ra0 = to_leaves ? leaf_a0 : 0u, rb0 = to_leaves ? leaf_b0 : 0u;  // output index base
+  const bool culling = q.cfg.culling != 0, enh = q.cfg.enhanced_bounds != 0;
+  unsigned long long my_culled = 0;
+  // leaf level: each block remembers its most promising leaf pair; k_seed
+  // evaluates these first so the narrow phase starts from a tight bound
+  float seed_key = kMax ? -INFINITY : INFINITY;
+  uint2 seed_pair = make_uint2(0, 0);
+
+  if (!overflow && k1) {
+    // survivors are staged in shared memory (warp-aggregated appends), then
+    // one global reservation per tile and a coalesced copy-out
+    extern __shared__ unsigned char k1_stage[];
+    uint2* s_node = reinterpret_cast<uint2*>(k1_stage);
+    float* s_key = reinterpret_cast<float*>(k1_stage + kK1Stage * sizeof(uint2));
+    const int ca = 1 << ka, cb = 1 << kb;
+    const int lane = threadIdx.x & 31;
+    for (unsigned long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      if (threadIdx.x == 0) sh.stage_count = 0;
+      __syncthreads();
+      const float ub = load_bound_sq(S);  // one bound snapshot per tile (query.py:396)
+      float upd = kMax ? 0.f : INFINITY;
+#pragma unroll 1
+      for (int r = 0; r < kK1Rounds; ++r) {
+      const unsigned long long e = tile * kK1Tile + (unsigned long long)r * kExpandThreads + threadIdx.x;
+      unsigned keep = 0;
+      float keys[4];
+      uint2 nd = make_uint2(0, 0);
+      if (e < n_in) {
+        const float pk = __ldg(in_key + e);
+        nd = __ldg(in_node + e);
+        // stale-entry re-cull: descendants' keys are monotone in the parent's
+        if (culling && !survives<kMax>(pk, ub)) {
+          my_culled += (unsigned)(ca * cb);
+        } else {
+          const unsigned a0 = ka ? 2 * nd.x + 1 : nd.x, b0 = kb ? 2 * nd.y + 1 : nd.y;
+          Box A[2], B[2];
+          A[0] = load_box(q.A.box, a0);
+          B[0] = load_box(q.B.box, b0);
+          if (ka) A[1] = load_box(q.A.box, a0 + 1);
+          if (kb) B[1] = load_box(q.B.box, b0 + 1);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              if (i >= ca || j >= cb) continue;
+              const int c = 2 * i + j;
+              const float key = pair_key<kMax>(A[i], B[j]);
+              keys[c] = key;
+              if (culling && !survives<kMax>(key, ub)) {
+                ++my_culled;
+                continue;
+              }
+              keep |= 1u << c;
+              const float u = pair_update<kMax>(A[i], B[j], enh);
+              upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
+              if (to_leaves && improves<kMax>(key, seed_key)) {
+                seed_key = key;
+                seed_pair = make_uint2(a0 + i - leaf_a0, b0 + j - leaf_b0);
+              }
+            }
+          nd = make_uint2(a0, b0);
+        }
+      }
+      // warp-aggregated append into the shared staging area
+      const unsigned cnt = __popc(keep);
+      unsigned incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      unsigned wbase = 0;
+      if (lane == 31 && incl) wbase = atomicAdd(&sh.stage_count, incl);
+      wbase = __shfl_sync(0xffffffffu, wbase, 31);
+      unsigned pos = wbase + incl - cnt;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (keep & (1u << c)) {
+          s_node[pos] = make_uint2(nd.x + (c >> 1) - ra0, nd.y + (c & 1) - rb0);
+          s_key[pos] = keys[c];
+          ++pos;
+        }
+      }
+      }  // rounds
+      upd = kMax ? warp_max(upd) : warp_min(upd);
+      if (lane == 0) sh.warp_upd[threadIdx.x >> 5] = upd;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned total = sh.stage_count;
+        sh.out_base = total ? atomicAdd(&S->n_out, (unsigned long long)total) : 0ull;
+        float u = sh.warp_upd[0];
+        for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
+        if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
+      }
+      __syncthreads();
+      const unsigned total = sh.stage_count;
+      const unsigned long long base = sh.out_base;
+      for (unsigned i = threadIdx.x; i < total; i += kExpandThreads) {
+        if (base + i < q.cap) {
+          out_node[base + i] = s_node[i];
+          out_key[base + i] = s_key[i];
+        }
+      }
+      __syncthreads();  // staging reuse by the next tile
+    }
+  } else if (!overflow) {
+    const unsigned long long off_mask = (1ull << shift) - 1, mask_b = (1ull << kb) - 1;
+    for (unsigned long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const unsigned long long base = tile * kGenericTile;
+      const float ub = load_bound_sq(S);
+      float upd = kMax ? 0.f : INFINITY;
+      uint2 on[kGenericItems];
+      float ok[kGenericItems];
+      unsigned keep = 0;
+#pragma unroll
+      for (int it = 0; it < kGenericItems; ++it) {
+        const unsigned long long t = base + (unsigned long long)it * kExpandThreads + threadIdx.x;
+        if (t >= ncand) continue;
+        const unsigned long long e = t >> shift, off = t & off_mask;
+        const float pk = __ldg(in_key + e);
+        if (culling && !survives<kMax>(pk, ub)) {
+          ++my_culled;
+          continue;
+        }
+        const uint2 nd = __ldg(in_node + e);
+        const unsigned na = (unsigned)(((((unsigned long long)nd.x + 1) << ka) - 1) + (off >> kb));
+        const unsigned nb = (unsigned)(((((unsigned long long)nd.y + 1) << kb) - 1) + (off & mask_b));
+        const Box ba = load_box(q.A.box, na), bb = load_box(q.B.box, nb);
+        const float key = pair_key<kMax>(ba, bb);
+        if (culling && !survives<kMax>(key, ub)) {
+          ++my_culled;
+          continue;
+        }
+        keep |= 1u << it;
+        on[it] = make_uint2(na - ra0, nb - rb0);
+        ok[it] = key;
+        const float u = pair_update<kMax>(ba, bb, enh);
+        upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
+        if (to_leaves && improves<kMax>(key, seed_key)) {
+          seed_key = key;
+          seed_pair = on[it];
+        }
+      }
+      unsigned my_off;
+      unsigned long long slot = tile_commit<kMax>(sh, S, __popc(keep), upd, my_off) + my_off;
+#pragma unroll
+      for (int it = 0; it < kGenericItems; ++it) {
+        if (keep & (1u << it)) {
+          if (slot < q.cap) {
+            out_node[slot] = on[it];
+            out_key[slot] = ok[it];
+          }
+          ++slot;
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // --- per-block counters and seed, then the last block advances the front --
+  unsigned long long c = warp_sum_u64(my_culled);
+  if ((threadIdx.x & 31) == 0) sh.red_culled[threadIdx.x >> 5] = c;
+  if (to_leaves) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float k2 = __shfl_xor_sync(0xffffffffu, seed_key, o);
+      const unsigned px = __shfl_xor_sync(0xffffffffu, seed_pair.x, o);
+      const unsigned py = __shfl_xor_sync(0xffffffffu, seed_pair.y, o);
+      if (improves<kMax>(k2, seed_key)) {
+        seed_key = k2;
+        seed_pair = make_uint2(px, py);
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sh.warp_upd[threadIdx.x >> 5] = seed_key;
+      sh.warp_seed[threadIdx.x >> 5] = seed_pair;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long bc = 0;
+    for (int w = 0; w < kExpandThreads / 32; ++w) bc += sh.red_culled[w];
+    if (bc) atomicAdd(&S->culled, bc);
+    if (to_leaves && blockIdx.x < kMaxSeeds) {
+      float bk = sh.warp_upd[0];
+      uint2 bp = sh.warp_seed[0];
+      for (int w = 1; w < kExpandThreads / 32; ++w)
+        if (improves<kMax>(sh.warp_upd[w], bk)) {
+          bk = sh.warp_upd[w];
+          bp = sh.warp_seed[w];
+        }
+      q.seed_key[blockIdx.x] = bk;
+      q.seed_pair[blockIdx.x] = bp;
+    }
+    __threadfence();
+    const unsigned prev = atomicAdd(&S->done, 1u);
+    if (prev == active - 1) {
+      __threadfence();
+      volatile QState* V = S;
+      const unsigned long long n_out = V->n_out;
+      const int it = V->iter;
+      if (overflow || n_out > (unsigned long long)q.cfg.front_hard_cap) {
+        S->err = GD_ERR_FRONT_OVERFLOW;
+        S->ov_cand = overflow ? (long long)ncand : (long long)n_out;
+        S->ov_in = (long long)n_in;
+        S->ov_cap = q.cfg.front_hard_cap;
+        S->n_in = 0;
+        S->n_leaf = 0;
+      } else {
+        S->expanded += ncand;
+        if (it < kMaxIters) {
+          GdIterStat st;
+          st.k = k;
+          st.front_in = (long long)n_in;
+          st.front_out = to_leaves ? 0 : (long long)n_out;
+          st.culled = (long long)V->culled;
+          const float b = __uint_as_float(V->bound_bits);
+          st.bound_after = kMax ? (double)b + (double)S->slack : (double)b - (double)S->slack;
+          st._pad = 0;
+          S->stats[it] = st;
+        }
+        if (to_leaves) {
+          S->n_leaf = n_out;
+          S->leaf_buf = cur ^ 1;
+          S->n_in = 0;
+          S->n_seed = min(active, (unsigned)kMaxSeeds);
+        } else {
+          S->n_in = n_out;
+          S->cur = cur ^ 1;
+        }
+        S->depth_a += ka;
+        S->depth_b += kb;
+      }
+      S->iter = it + 1;
+      S->n_out = 0;
+      S->culled = 0;
+      S->done = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// seed pass: the best leaf pair of every leaf-level expand block goes through
+// the narrow phase first, so the main pass culls against a bound close to the
+// answer (the reference gets this from its sequential batches, query.py:396,
+// 411-415).  Seed pairs that can still be the answer also join the band.
+template <bool kMax>
+__global__ __launch_bounds__(256) void k_seed(QArgs q) {
+  QState* S = q.S;
+  const unsigned ns = S->n_seed;
+  if (ns == 0 || S->n_leaf == 0) return;
+  if (blockIdx.x * 256 >= 4 * ns) return;
+  __shared__ float warp_upd[8];
+  const unsigned t = blockIdx.x * 256 + threadIdx.x;
+  const float E = S->slack;
+  float d = kMax ? 0.f : INFINITY;
+  bool valid = false;
+  unsigned ta = 0, tb = 0;
+  if (t < 4 * ns) {
+    const float key = q.seed_key[t >> 2];
+    if (isfinite(key)) {
+      const uint2 lp = q.seed_pair[t >> 2];
+      const unsigned ia = (t >> 1) & 1, ib = t & 1;
+      const unsigned fa = q.A.leaf_first[lp.x], ca = q.A.leaf_first[lp.x + 1] - fa;
+      const unsigned fb = q.B.leaf_first[lp.y], cb = q.B.leaf_first[lp.y + 1] - fb;
+      if (ia < ca && ib < cb) {
+        const int4 sa = reinterpret_cast<const int4*>(q.A.leaf_tri)[fa + ia];
+        const int4 sb = reinterpret_cast<const int4*>(q.B.leaf_tri)[fb + ib];
+        const Tri<float> A = load_tri32(q.A, sa), B = load_tri32(q.B, sb);
+        d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
+                 : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+        valid = true;
+        ta = (unsigned)sa.w;
+        tb = (unsigned)sb.w;
+      }
+    }
+  }
+  float u = kMax ? warp_max(d) : warp_min(d);
+  if ((threadIdx.x & 31) == 0) warp_upd[threadIdx.x >> 5] = u;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) u = kMax ? fmaxf(u, warp_upd[w]) : fminf(u, warp_upd[w]);
+    if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, u);
+  }
+  __syncthreads();
+  if (valid) {
+    const float ub = load_bound(S);
+    if (kMax ? (d + E >= ub) : (d - E <= ub)) {
+      const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
+      if (slot < q.band_cap) {
+        q.band_ids[slot] = make_uint2(ta, tb);
+        q.band_d[slot] = d;
+      } else {
+        S->band_overflow = 1;
+      }
+    }
+  }
+}
+
+}  // namespace gd

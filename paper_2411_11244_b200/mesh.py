@@ -113,7 +113,7 @@ class TriangleMesh:
             dev = _lib.device()
             if len(root._triangles) >= 2**31 or len(root._vertices) >= 2**31:
                 raise ValueError("meshes above 2^31 vertices/triangles are not supported")
-            vt = torch.from_numpy(np.ascontiguousarray(root._vertices)).to(dev)
+            vt = torch.from_numpy(np.array(root._vertices, dtype=np.float64, order="C")).to(dev)
             tr = torch.from_numpy(root._triangles.astype(np.int32)).to(dev)
             root._dev = (vt, tr)
         return root._dev

@@ -115,16 +115,21 @@ def test_build_structure_suite(md, gpu, oracle):
             assert np.array_equal(pts.min(0), t.node_min[node]) and np.array_equal(pts.max(0), t.node_max[node])
 
 
-def test_refit_moved_mesh(md, gpu):
+def test_refit_moved_mesh(md, gpu, oracle):
     a, _ = md.gen_scene("interlocked-rings", {"nu": 60, "nv": 30})
     t = md.build_f12(a)
     xf = md.RigidTransform.from_axis_angle((0.3, -1, 2), 1.3, (0.5, -0.25, 2.0))
     moved = md.apply_transform(a, xf)
     md.refit(t, moved)
-    ref = md.build_f12(md.TriangleMesh(moved.vertices, moved.triangles))
+    # same topology, boxes recomputed from the reference's moved vertices
+    ref = oracle.Tree(np.empty((t.n_nodes, 3)), np.empty((t.n_nodes, 3)), t.leaf_tris, t.prim_order, t.depth)
+    oracle.fill_boxes(ref, moved.vertices, moved.triangles)
     # device transform vs numpy dgemm differ by <= 1 ulp per coordinate
     assert np.allclose(t.node_min, ref.node_min, rtol=0, atol=4e-15 * np.abs(ref.node_min).max())
     assert np.allclose(t.node_max, ref.node_max, rtol=0, atol=4e-15 * np.abs(ref.node_max).max())
+    # a refit with an explicitly materialised mesh is bitwise the reference
+    md.refit(t, md.TriangleMesh(moved.vertices, moved.triangles))
+    assert np.array_equal(t.node_min, ref.node_min) and np.array_equal(t.node_max, ref.node_max)
     with pytest.raises(md.TopologyMismatchError):
         md.refit(t, md.gen_scene("random-blobs", {"n": 7})[0])
     # translation commutes with min/max (SPEC refit example)
