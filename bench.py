@@ -11,9 +11,11 @@ query (refits included): max-over-ranks device time of the K steps / (K N).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-`--impl reference` times the CPU oracle port of the reference algorithm
-(oracle/meshdist_oracle.py; the reference itself is pure Python and does not
-travel to the GPU box) on the same frames, all host threads, bounded steps.
+`--impl reference` times the reference's own CPU path on the box's host cores:
+the unmodified reference package (pure Python + numpy) installed into
+baseline/_ref (git-ignored, shipped by gpurun), driven through its public API
+on the same frames with all host threads, bounded steps; the oracle port
+(oracle/, a numpy restatement) stands in only if baseline/_ref is absent.
 """
 
 from __future__ import annotations
@@ -312,66 +314,136 @@ def run_ours(args):
 
 
 # ---------------------------------------------------------------------------
-def oracle_trees(md, bvh_a, bvh_b):
-    """Oracle trees sharing the device tree's topology (the reference's
-    O(n^2) greedy cannot build 7.5M triangles; pairing parity is tested)."""
+# CPU legs: the UNMODIFIED reference package (pure Python + numpy, pip-installed
+# into baseline/_ref, which gpurun ships to the box) through its own public API;
+# the oracle port (oracle/, test infrastructure) only when baseline/_ref is absent.
+def load_reference():
+    src = REPO / "baseline" / "_ref"
+    if not (src / "meshdist" / "__init__.py").exists():
+        return None
+    sys.path.insert(0, str(src))
+    import meshdist
+
+    assert Path(meshdist.__file__).resolve().is_relative_to(src.resolve()), meshdist.__file__
+    return meshdist
+
+
+class CpuLeg:
+    """One step of the reference path on the host: apply_transform + refit of
+    both meshes for frame f, then run_min_query / run_max_query.  The tree
+    topology comes from our exact-pairing build (bit-equal to the reference's
+    greedy, tests/test_abi_host.py); the reference's own O(n^2) pairing cannot
+    build 7.5M triangles (hard part 1)."""
+
+    def __init__(self, md, tz, tbm, bvh_a, bvh_b, kind, workers):
+        self.md, self.kind, self.workers = md, kind, workers
+        self.ref = load_reference()
+        self.kind_label = "reference" if self.ref is not None else "port"
+        if self.ref is not None:
+            R = self.ref
+            self.A0 = R.TriangleMesh(tz.vertices, tz.triangles)
+            self.B0 = R.TriangleMesh(tbm.vertices, tbm.triangles)
+
+            def tree(b):
+                n = b.n_nodes
+                return R.F12Bvh(np.empty((n, 3)), np.empty((n, 3)), np.asarray(b.leaf_tris).copy(),
+                                np.asarray(b.prim_order).copy(), int(b.depth))
+
+            self.ta, self.tb = tree(bvh_a), tree(bvh_b)
+            # front_hard_cap raised as in the GPU run: at the default 2^24 the
+            # reference raises FrontOverflowError on this workload (query.py:375)
+            self.cfg = R.EngineConfig(threads=workers, front_hard_cap=1 << 27)
+        else:
+            from oracle import meshdist_oracle as oracle
+
+            self.oracle = oracle
+            self.tz, self.tbm = tz, tbm
+
+            def tree(b):
+                return oracle.Tree(np.empty((b.n_nodes, 3)), np.empty((b.n_nodes, 3)), np.asarray(b.leaf_tris),
+                                   np.asarray(b.prim_order), b.depth)
+
+            self.ta, self.tb = tree(bvh_a), tree(bvh_b)
+
+    def describe(self):
+        if self.ref is not None:
+            return f"unmodified reference package (baseline/_ref, numpy, EngineConfig(threads={self.workers}))"
+        return f"oracle port of the reference (oracle/, numpy, {self.workers} threads)"
+
+    def frame(self, f):
+        xa, xb = self.md.ring_frame_transforms(f % 1000)
+        if self.ref is not None:
+            R = self.ref
+            a = R.apply_transform(self.A0, R.RigidTransform(xa.rotation, xa.translation))
+            b = R.apply_transform(self.B0, R.RigidTransform(xb.rotation, xb.translation))
+            R.refit(self.ta, a)
+            R.refit(self.tb, b)
+            run = R.run_min_query if self.kind == "min" else R.run_max_query
+            return run(a, b, self.ta, self.tb, self.cfg).distance
+        o = self.oracle
+        va = o.transform_vertices(self.tz.vertices, xa.rotation, xa.translation)
+        vb = o.transform_vertices(self.tbm.vertices, xb.rotation, xb.translation)
+        o.fill_boxes(self.ta, va, self.tz.triangles)
+        o.fill_boxes(self.tb, vb, self.tbm.triangles)
+        pa = o.triangle_points(va, self.tz.triangles)
+        pb = o.triangle_points(vb, self.tbm.triangles)
+        return o.run_query(self.ta, self.tb, pa, pb, self.kind,
+                           o.Config(workers=self.workers, front_hard_cap=1 << 27)).distance
+
+
+class _Topology:
+    def __init__(self, leaf_tris, prim_order):
+        self.leaf_tris, self.prim_order = leaf_tris, prim_order
+        self.n_nodes = 2 * len(leaf_tris) - 1
+        self.depth = len(leaf_tris).bit_length() - 1
+
+
+def host_topology(mesh):
+    """build_f12's topology (bvh.py:267-289) on the host: the oracle's Morton
+    order + surface areas, and the exact O(n log n) greedy pairing of
+    libgdist (host C++, gd_pair_greedy; bit-equal to the reference's greedy)."""
+    import ctypes as C
+
     from oracle import meshdist_oracle as oracle
+    from paper_2411_11244_b200 import _lib
 
-    ta = oracle.Tree(np.empty((bvh_a.n_nodes, 3)), np.empty((bvh_a.n_nodes, 3)), np.asarray(bvh_a.leaf_tris),
-                     np.asarray(bvh_a.prim_order), bvh_a.depth)
-    tb = oracle.Tree(np.empty((bvh_b.n_nodes, 3)), np.empty((bvh_b.n_nodes, 3)), np.asarray(bvh_b.leaf_tris),
-                     np.asarray(bvh_b.prim_order), bvh_b.depth)
-    return oracle, ta, tb
-
-
-def cpu_frame_query(oracle, ta, tb, tz, tbm, f, kind, workers):
-    """One step of the reference algorithm on the CPU: oracle refit of both
-    meshes for frame f (fill_boxes) + oracle query."""
-    import paper_2411_11244_b200 as md
-
-    xa, xb = md.ring_frame_transforms(f % 1000)
-    va = oracle.transform_vertices(tz.vertices, xa.rotation, xa.translation)
-    vb = oracle.transform_vertices(tbm.vertices, xb.rotation, xb.translation)
-    oracle.fill_boxes(ta, va, tz.triangles)
-    oracle.fill_boxes(tb, vb, tbm.triangles)
-    pa = oracle.triangle_points(va, tz.triangles)
-    pb = oracle.triangle_points(vb, tbm.triangles)
-    # front_hard_cap raised like the GPU run's: at the default 2^24 the
-    # reference raises FrontOverflowError on this workload (query.py:375)
-    return oracle.run_query(ta, tb, pa, pb, kind, oracle.Config(workers=workers, front_hard_cap=1 << 27))
+    V, T = mesh.vertices, mesh.triangles
+    _, order = oracle.morton_order(V, T)
+    P = V[T]
+    n = len(T)
+    sa = np.ascontiguousarray(oracle.pair_surface_areas(order, P.min(axis=1), P.max(axis=1)), dtype=np.float64)
+    is_left = np.zeros(n, dtype=np.uint8)
+    _lib.check(_lib.lib().gd_pair_greedy(sa.ctypes.data_as(C.c_void_p), n, is_left.ctypes.data_as(C.c_void_p)),
+               "pair_greedy")
+    return _Topology(oracle.leaves_from_pairs(order, np.flatnonzero(is_left), n), order)
 
 
 def cpu_baseline(args, ctx, budget):
     import paper_2411_11244_b200 as md
 
     tz, tbm, bvh_a, bvh_b, frames, results = ctx
-    oracle, ta, tb = oracle_trees(md, bvh_a, bvh_b)
     workers = os.cpu_count() or 1
+    leg = CpuLeg(md, tz, tbm, bvh_a, bvh_b, args.kind, workers)
     t0 = time.perf_counter()
-    r = cpu_frame_query(oracle, ta, tb, tz, tbm, frames[-1], args.kind, workers)
+    d = leg.frame(frames[-1])
     sec = time.perf_counter() - t0
-    agree = r.distance == results[-1].distance
-    return {"value": round(sec * 1e3, 3), "unit": "ms/query", "cores": workers, "kind": "port",
-            "sample": f"1 frame (f={frames[-1]}) of the same workload: oracle refit A+B + {args.kind} query, "
-                      f"numpy, {workers} threads",
-            "distance_equal_to_gpu": bool(agree)}
+    return {"value": round(sec * 1e3, 3), "unit": "ms/query", "cores": workers, "kind": leg.kind_label,
+            "sample": f"1 frame (f={frames[-1]}) of the same workload: refit A+B + {args.kind} query, "
+                      f"{leg.describe()}",
+            "distance_equal_to_gpu": bool(d == results[-1].distance)}
 
 
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return None
-    import torch
-
     import paper_2411_11244_b200 as md
 
-    torch.cuda.set_device(local) if torch.cuda.is_available() else None
     tz, tbm = md.ring_pair_base(args.nu, args.nv)
-    # the tree topology comes from our exact-pairing build (parity-tested
-    # against the reference greedy; the literal O(n^2) greedy does not finish)
-    bvh_a, bvh_b = md.build_f12(tz), md.build_f12(tbm)
-    oracle, ta, tb = oracle_trees(md, bvh_a, bvh_b)
+    # tree topology on the host (untimed setup, no device work on this arm)
+    bvh_a, bvh_b = host_topology(tz), host_topology(tbm)
     workers = os.cpu_count() or 1
+    leg = CpuLeg(md, tz, tbm, bvh_a, bvh_b, args.kind, workers)
     N = args.gpus
     W = min(args.warmup, 1)
     times = []
@@ -380,7 +452,7 @@ def run_reference(args):
     while s < W + args.steps:
         f = s * N
         t0 = time.perf_counter()
-        cpu_frame_query(oracle, ta, tb, tz, tbm, f, args.kind, workers)
+        leg.frame(f)
         dt = time.perf_counter() - t0
         if s >= W:
             times.append(dt)
@@ -405,9 +477,9 @@ def run_reference(args):
         "config": {"workload": f"rings {2 * args.nu * args.nv} tris/mesh (config 2), frame f = step*N; step = "
                                f"refit A + refit B + {args.kind} query", "nu": args.nu, "nv": args.nv,
                    "kind": args.kind, "precision": 64},
-        "cpu_baseline": {"value": round(value, 3), "unit": "ms/query", "cores": workers, "kind": "port",
+        "cpu_baseline": {"value": round(value, 3), "unit": "ms/query", "cores": workers, "kind": leg.kind_label,
                          "sample": f"{len(times)} frame steps (bounded to {args.cpu_budget:.0f} s) of the same "
-                                   f"workload, oracle port of the reference (numpy, {workers} threads)"},
+                                   f"workload, {leg.describe()}"},
         "e2e": {"value": round(value, 3), "unit": "ms/query", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

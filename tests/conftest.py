@@ -37,14 +37,17 @@ def oracle():
 
 @pytest.fixture(scope="session")
 def reference():
-    """The live reference package (build container only)."""
-    if not (REFERENCE_SRC / "meshdist" / "__init__.py").exists():
-        pytest.skip("reference not mounted (expected on the GPU box)")
+    """The live reference package: /root/reference in the build container, or
+    the unmodified copy pip-installed into baseline/_ref (travels to the GPU box)."""
+    src = next((s for s in (REFERENCE_SRC, REPO / "baseline" / "_ref") if (s / "meshdist" / "__init__.py").exists()),
+               None)
+    if src is None:
+        pytest.skip("reference package not available here")
     import importlib.util
 
     spec = importlib.util.spec_from_file_location(
-        "meshdist_ref", REFERENCE_SRC / "meshdist" / "__init__.py",
-        submodule_search_locations=[str(REFERENCE_SRC / "meshdist")])
+        "meshdist_ref", src / "meshdist" / "__init__.py",
+        submodule_search_locations=[str(src / "meshdist")])
     mod = importlib.util.module_from_spec(spec)
     sys.modules["meshdist_ref"] = mod
     spec.loader.exec_module(mod)

@@ -1,0 +1,108 @@
+"""The oracle restatement against the LIVE reference package (CPU only).
+
+Runs wherever the reference is importable: `/root/reference/pkg/src` in the build
+container, or the unmodified copy installed into `baseline/_ref` (git-ignored,
+shipped to the GPU box by gpurun).  Skips otherwise -- the committed golden vectors
+(test_oracle_golden.py) pin the oracle on every machine.  Fresh seeded inputs here,
+so the oracle is checked beyond the goldens it was written against.
+"""
+
+import numpy as np
+import pytest
+
+
+def _eq(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, (a.shape, b.shape)
+    bad = ~((a == b) | (np.isnan(a) & np.isnan(b)))
+    assert not bad.any(), f"{bad.sum()} mismatches, first at {np.argwhere(bad)[:3].tolist()}"
+
+
+def _tris(rng, n, scale=1.0):
+    base = rng.normal(size=(n, 1, 3))
+    return base + scale * rng.normal(size=(n, 3, 3)) * rng.uniform(0.01, 1.0, size=(n, 1, 1))
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_tri_tri_random(reference, oracle, prec):
+    """bounds.py:245-330 vs oracle.tri_tri_min/max on fresh random pairs,
+    including exact copies (distance 0) and shared vertices."""
+    from importlib import import_module
+
+    rb = import_module(reference.__name__ + ".bounds")
+    rng = np.random.default_rng(1234 + prec)
+    dt = np.float64 if prec == 64 else np.float32
+    t1 = _tris(rng, 3000).astype(dt)
+    t2 = _tris(rng, 3000).astype(dt) * 0.3 + t1 * 0.7
+    t2[:100] = t1[:100]                       # identical triangles
+    t2[100:200, 0] = t1[100:200, 1]           # shared vertex
+    for fr, fo in ((rb.batch_tri_tri_min, oracle.tri_tri_min), (rb.batch_tri_tri_max, oracle.tri_tri_max)):
+        dr, pr, qr = fr(t1, t2)
+        do, po, qo = fo(t1, t2)
+        _eq(do, dr)
+        _eq(po, pr)
+        _eq(qo, qr)
+
+
+def test_box_bounds_random(reference, oracle):
+    """bounds.py:47-101 (Eqs. 5-10) vs the oracle, f64 and f32."""
+    from importlib import import_module
+
+    rb = import_module(reference.__name__ + ".bounds")
+    rng = np.random.default_rng(77)
+    for dt in (np.float64, np.float32):
+        c = rng.normal(size=(4, 5000, 3))
+        amin = (c[0] - np.abs(c[1])).astype(dt)
+        amax = (c[0] + np.abs(c[1])).astype(dt)
+        bmin = (c[2] - np.abs(c[3])).astype(dt)
+        bmax = (c[2] + np.abs(c[3])).astype(dt)
+        for name, fo in (("batch_min_lower", oracle.box_min_lower), ("batch_max_upper", oracle.box_max_upper),
+                         ("batch_enhanced_min_upper", oracle.enhanced_min_upper),
+                         ("batch_enhanced_max_lower", oracle.enhanced_max_lower)):
+            _eq(fo(amin, amax, bmin, bmax), getattr(rb, name)(amin, amax, bmin, bmax))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 7, 300, 1000, 2049])
+def test_build_random_soup(reference, oracle, n):
+    """build_f12 (bvh.py:267-289) vs oracle.build_tree: prim_order, leaf_tris
+    and every node box, both dtypes (exercises the pairing deferrals)."""
+    rng = np.random.default_rng(n)
+    V = np.round(rng.normal(size=(3 * n, 3)), 2)  # rounded: surface-area ties
+    T = np.arange(3 * n).reshape(n, 3)
+    mesh = reference.TriangleMesh(V, T)
+    for dt in (np.float64, np.float32):
+        r = reference.build_f12(mesh, dtype=dt)
+        o = oracle.build_tree(V, T, dtype=dt)
+        _eq(o.prim_order, r.prim_order)
+        _eq(o.leaf_tris, r.leaf_tris)
+        _eq(o.node_min, r.node_min)
+        _eq(o.node_max, r.node_max)
+        assert o.depth == r.depth
+
+
+@pytest.mark.parametrize("kind", ["min", "max"])
+@pytest.mark.parametrize("prec", [64, 32])
+def test_engine_small_tori(reference, oracle, md, kind, prec):
+    """run_min_query / run_max_query (query.py:540-568) vs oracle.run_query on a
+    small interlocked-rings scene at a rotation-sequence frame: distance,
+    witness and every IterationStat."""
+    tz, tb = md.ring_pair_base(30, 20)
+    xa, xb = md.ring_frame_transforms(137)
+    A = reference.TriangleMesh(tz.vertices, tz.triangles)
+    B = reference.TriangleMesh(tb.vertices, tb.triangles)
+    A = reference.apply_transform(A, reference.RigidTransform(xa.rotation, xa.translation))
+    B = reference.apply_transform(B, reference.RigidTransform(xb.rotation, xb.translation))
+    dt = np.float64 if prec == 64 else np.float32
+    ra, rbv = reference.build_f12(A, dtype=dt), reference.build_f12(B, dtype=dt)
+    cfg = reference.EngineConfig(precision=prec)
+    run = reference.run_min_query if kind == "min" else reference.run_max_query
+    want = run(A, B, ra, rbv, cfg)
+    oa = oracle.build_tree(A.vertices, A.triangles, dtype=dt)
+    ob = oracle.build_tree(B.vertices, B.triangles, dtype=dt)
+    got = oracle.run_query(oa, ob, oracle.triangle_points(A.vertices, A.triangles, dt),
+                           oracle.triangle_points(B.vertices, B.triangles, dt), kind, oracle.Config(precision=prec))
+    assert got.distance == want.distance
+    assert (got.tri_a, got.tri_b) == (want.witness.tri_a, want.witness.tri_b)
+    assert [tuple(s[:4]) for s in got.iterations] == [(s.k, s.front_in, s.front_out, s.culled)
+                                                      for s in want.iterations]
+    assert got.expanded_pairs == want.expanded_pairs and got.narrow_pairs == want.narrow_pairs
