@@ -64,8 +64,10 @@ typedef struct GdBvhSizes {
 /* Device-resident f12-BVH (bvh.py:184-239).  Storage is implicit BFS: node
  * i has children 2i+1, 2i+2; leaves are the last L nodes.  All arrays are
  * caller-allocated device memory:
- *   box        : n_nodes * 6 float32  (minx,miny,minz,maxx,maxy,maxz) per node,
- *                traversal boxes of the float32-rounded vertices
+ *   box        : (n_nodes + 1) * 6 float32 (minx,miny,minz,maxx,maxy,maxz);
+ *                node i at slot i + 1 (slot 0 is padding, so each sibling
+ *                pair starts 16-byte aligned); traversal boxes of the
+ *                float32-rounded vertices
  *   leaf_tri   : m * 4 int32  {v0, v1, v2, triangle id} in leaf (Morton) order
  *   leaf_first : (L + 1) uint32, first leaf_tri slot of each leaf
  *   vtx32      : nv * 4 float32, transformed float32 vertices (refit output)  */
@@ -133,7 +135,8 @@ int gd_device_count(int* count);
 /* number of hot-path kernels (refit + query) launched by this process */
 long long gd_launch_count(void);
 /* phase timing of subsequent queries (CUDA events); gd_query_phase_ms
- * returns the count written: [init, expand, narrow, exact pass, final] ms */
+ * returns the count written: [init, expand, narrow, exact pass, final] ms,
+ * then (n > 5) the duration of each k_expand launch of the last query */
 int gd_set_profiling(int enable);
 int gd_query_phase_ms(float* out, int n);
 

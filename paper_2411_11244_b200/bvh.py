@@ -53,7 +53,7 @@ class Aabb:
 class F12Bvh:
     """Full binary AABB tree in implicit BFS storage (bvh.py:184-239).
 
-    Device state: `_box` (n_nodes x 6 float32 traversal boxes), `_leaf_tri`
+    Device state: `_box` ((n_nodes + 1) x 6 float32 traversal boxes, node i at slot i + 1), `_leaf_tri`
     (m x int4 leaf-ordered slots), `_leaf_first` (L + 1), `_vtx32`.
     Host state: `leaf_tris` (L, 2) int64, `prim_order` (m,) int64, `depth`.
     """
@@ -148,7 +148,7 @@ class F12Bvh:
         torch = _lib.torch()
         L = self.leaf_count
         m = len(self.prim_order)
-        self._box = _lib.empty((2 * L - 1) * 6, torch.float32)
+        self._box = _lib.empty(2 * L * 6, torch.float32)  # slot 0 = padding (gdist.h)
         self._leaf_tri = _lib.empty(m * 4, torch.int32)
         self._leaf_first = _lib.empty(L + 1, torch.int32)
         self._vtx32 = _lib.empty(max(nv, 1) * 4, torch.float32)

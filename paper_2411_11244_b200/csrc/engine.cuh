@@ -18,13 +18,17 @@ struct alignas(16) QState {
   int iter;
   int leaf_buf;                      // buffer holding the leaf-pair list
   unsigned long long n_in, n_out, n_leaf, n_band;
+  unsigned long long n_cand;         // triangle-pair candidates (k_nfilter)
   unsigned long long expanded, narrow, culled, band_eval;
   long long ov_cand, ov_in, ov_cap;
   float slack;
   int band_overflow;
   unsigned n_seed;                   // blocks that wrote a seed leaf pair
-  int _pad2;
+  unsigned bar;                      // grid-barrier arrivals (k_traverse)
+  unsigned long long cnt[kMaxIters + 1];       // survivors written by iteration i
+  unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
   GdIterStat stats[kMaxIters];
+  unsigned long long t_it[kMaxIters + 1];      // %globaltimer at iteration boundaries
 };
 
 constexpr int kMaxSeeds = 8192;
@@ -45,20 +49,41 @@ struct QArgs {
   GdResult* result;             // device result record
 };
 
-// 24-byte AoS node box: (minx,miny,minz,maxx,maxy,maxz), float2-aligned.
+// 24-byte AoS node boxes (minx,miny,minz,maxx,maxy,maxz), stored at slot
+// node + 1 (slot 0 is padding): the sibling pair (2i+1, 2i+2) then starts at
+// byte 48 (i + 1), 16-byte aligned, and loads as three float4.
 __device__ __forceinline__ Box load_box(const float* __restrict__ box, unsigned long long node) {
-  const float2* p = reinterpret_cast<const float2*>(box + node * 6);
+  const float2* p = reinterpret_cast<const float2*>(box + (node + 1) * 6);
   float2 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
   Box r;
   r.lo[0] = a.x; r.lo[1] = a.y; r.lo[2] = b.x;
   r.hi[0] = b.y; r.hi[1] = c.x; r.hi[2] = c.y;
   return r;
 }
+// both children of `parent` (nodes 2 parent + 1, 2 parent + 2)
+__device__ __forceinline__ void load_children(const float* __restrict__ box, unsigned long long parent, Box& c0,
+                                              Box& c1) {
+  const float4* p = reinterpret_cast<const float4*>(box + (2 * parent + 2) * 6);
+  const float4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+  c0.lo[0] = a.x; c0.lo[1] = a.y; c0.lo[2] = a.z;
+  c0.hi[0] = a.w; c0.hi[1] = b.x; c0.hi[2] = b.y;
+  c1.lo[0] = b.z; c1.lo[1] = b.w; c1.lo[2] = c.x;
+  c1.hi[0] = c.y; c1.hi[1] = c.z; c1.hi[2] = c.w;
+}
 __device__ __forceinline__ void store_box(float* box, unsigned long long node, const Box& r) {
-  float2* p = reinterpret_cast<float2*>(box + node * 6);
+  float2* p = reinterpret_cast<float2*>(box + (node + 1) * 6);
   p[0] = make_float2(r.lo[0], r.lo[1]);
   p[1] = make_float2(r.lo[2], r.hi[0]);
   p[2] = make_float2(r.hi[1], r.hi[2]);
+}
+__device__ __forceinline__ Box select_box(bool c, const Box& a, const Box& b) {
+  Box r;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    r.lo[k] = c ? a.lo[k] : b.lo[k];
+    r.hi[k] = c ? a.hi[k] : b.hi[k];
+  }
+  return r;
 }
 __device__ __forceinline__ Box box_union(const Box& a, const Box& b) {
   Box r;

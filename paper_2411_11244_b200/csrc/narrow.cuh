@@ -40,6 +40,25 @@ __device__ __forceinline__ Key128 shfl_key(Key128 k, int o) {
   return r;
 }
 
+// Lower bound^2 of the distance between two triangles: the gap between their
+// projections on the axis through the centroids (any axis separates at most
+// by the distance).  float32, well inside the slack E.
+__device__ __forceinline__ float axis_gap_sq(const Tri<float>& a, const Tri<float>& b) {
+  const float nx = (b.v[0].x + b.v[1].x + b.v[2].x) - (a.v[0].x + a.v[1].x + a.v[2].x);
+  const float ny = (b.v[0].y + b.v[1].y + b.v[2].y) - (a.v[0].y + a.v[1].y + a.v[2].y);
+  const float nz = (b.v[0].z + b.v[1].z + b.v[2].z) - (a.v[0].z + a.v[1].z + a.v[2].z);
+  const float n2 = fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+  if (!(n2 > 0.f)) return 0.f;
+  float amax = -INFINITY, bmin = INFINITY;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    amax = fmaxf(amax, fmaf(a.v[i].x, nx, fmaf(a.v[i].y, ny, a.v[i].z * nz)));
+    bmin = fminf(bmin, fmaf(b.v[i].x, nx, fmaf(b.v[i].y, ny, b.v[i].z * nz)));
+  }
+  const float g = bmin - amax;  // gap * |n|
+  return g > 0.f ? g * g / n2 : 0.f;
+}
+
 // ---------------------------------------------------------------------------
 // fast float32 narrow phase over the leaf-pair list: every leaf pair expands
 // to its 1..4 triangle pairs inside the block (block scan), a triangle-box
@@ -104,8 +123,13 @@ __global__ __launch_bounds__(kNarrowThreads) void k_narrow(QArgs q) {
       const uint2 f = s_first[o];
       const int4 sa = __ldg(lta + f.x + j / cbo);
       const int4 sb = __ldg(ltb + f.y + j % cbo);
-      const Box ba = tri_box(load_tri32(q.A, sa)), bb = tri_box(load_tri32(q.B, sb));
-      if (!culling || survives<kMax>(pair_key<kMax>(ba, bb), ub1)) work[atomicAdd(&n_work, 1u)] = (unsigned short)s;
+      const Tri<float> ta = load_tri32(q.A, sa), tb = load_tri32(q.B, sb);
+      bool keep = !culling || survives<kMax>(pair_key<kMax>(tri_box(ta), tri_box(tb)), ub1);
+      // min query: separating-axis lower bound along the centroid axis --
+      // near contact it is within a triangle's thickness of the distance,
+      // where the box bound loses a whole triangle extent
+      if (!kMax && culling && keep) keep = axis_gap_sq(ta, tb) <= ub1;
+      if (keep) work[atomicAdd(&n_work, 1u)] = (unsigned short)s;
     }
     __syncthreads();
     const unsigned nw = n_work;
@@ -155,6 +179,154 @@ __global__ __launch_bounds__(kNarrowThreads) void k_narrow(QArgs q) {
     __syncthreads();
   }
   if (!kRescan && threadIdx.x == 0 && my_pairs) atomicAdd(&S->narrow, my_pairs);
+}
+
+// ---------------------------------------------------------------------------
+// Narrow phase, stage 1 (k_nfilter): one thread per leaf pair.  Re-culls the
+// pair with the (seeded) bound, loads its 1..2 x 1..2 triangles once, and
+// keeps the triangle pairs whose box bound -- and, for min queries, the
+// centroid-axis separation bound -- can still beat the bound.  Survivors
+// (leaf-slot index pairs) are appended, warp-aggregated, to the idle front
+// buffer; stage 2 (k_ntest) runs the full test on that dense list.
+template <bool kMax>
+__global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
+  QState* S = q.S;
+  const unsigned long long n = S->n_leaf;
+  if (n == 0) return;
+  const int buf = S->leaf_buf;
+  const uint2* leaves = q.node[buf];
+  const float* keys = q.key[buf];
+  uint2* out = q.node[buf ^ 1];
+  const bool culling = q.cfg.culling != 0;
+  const int4* __restrict__ lta = reinterpret_cast<const int4*>(q.A.leaf_tri);
+  const int4* __restrict__ ltb = reinterpret_cast<const int4*>(q.B.leaf_tri);
+  const int lane = threadIdx.x & 31;
+  const float E = S->slack;
+  float upd = 0.f;  // max query only
+  unsigned long long tested = 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const unsigned long long i = base + threadIdx.x;
+    const float ub = load_bound(S), ub2 = ub * ub;
+    unsigned mask = 0;
+    unsigned fa = 0, fb = 0;
+    if (i < n && (!culling || survives<kMax>(keys[i], ub2))) {
+      const uint2 lp = leaves[i];
+      fa = __ldg(q.A.leaf_first + lp.x);
+      const unsigned ca = __ldg(q.A.leaf_first + lp.x + 1) - fa;
+      fb = __ldg(q.B.leaf_first + lp.y);
+      const unsigned cb = __ldg(q.B.leaf_first + lp.y + 1) - fb;
+      Tri<float> ta[2], tb[2];
+      ta[0] = load_tri32(q.A, __ldg(lta + fa));
+      tb[0] = load_tri32(q.B, __ldg(ltb + fb));
+      if (ca > 1) ta[1] = load_tri32(q.A, __ldg(lta + fa + 1));
+      if (cb > 1) tb[1] = load_tri32(q.B, __ldg(ltb + fb + 1));
+#pragma unroll
+      for (int ia = 0; ia < 2; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < 2; ++ib) {
+          if (ia >= (int)ca || ib >= (int)cb) continue;
+          bool keep = !culling || survives<kMax>(pair_key<kMax>(tri_box(ta[ia]), tri_box(tb[ib])), ub2);
+          if (!kMax && culling && keep) keep = axis_gap_sq(ta[ia], tb[ib]) <= ub2;
+          if (kMax && keep) {
+            // max query: the exact test is 9 vertex pairs -- cheaper here, on
+            // the loaded triangles, than a candidate round trip
+            const float d = sqrtf(tri_tri_max_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr));
+            upd = fmaxf(upd, d);
+            ++tested;
+            if (d + E >= ub) {
+              const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
+              if (slot < q.band_cap) {
+                q.band_ids[slot] = make_uint2((unsigned)__ldg(lta + fa + ia).w, (unsigned)__ldg(ltb + fb + ib).w);
+                q.band_d[slot] = d;
+              } else {
+                S->band_overflow = 1;
+              }
+            }
+            keep = false;
+          }
+          if (keep) mask |= 1u << (2 * ia + ib);
+        }
+    }
+    // warp-aggregated append of up to 4 slot pairs per thread
+    const unsigned cnt = __popc(mask);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    unsigned long long wbase = 0;
+    if (lane == 31 && incl) wbase = atomicAdd(&S->n_cand, (unsigned long long)incl);
+    wbase = __shfl_sync(0xffffffffu, wbase, 31);
+    unsigned long long pos = wbase + incl - cnt;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (mask & (1u << c)) {
+        if (pos < q.cap)
+          out[pos] = make_uint2(fa + (c >> 1), fb + (c & 1));
+        else
+          S->band_overflow = 1;  // k_narrow<rescan> re-scans every leaf pair exactly
+        ++pos;
+      }
+    }
+  }
+  if (kMax) {
+    upd = warp_max(upd);
+    tested = warp_sum_u64(tested);
+    if (lane == 0) {
+      if (upd > 0.f) commit_bound<kMax>(S, upd);
+      if (tested) atomicAdd(&S->narrow, tested);
+    }
+  }
+}
+
+// Narrow phase, stage 2 (k_ntest): the float32 triangle-pair test on the
+// dense candidate list; updates the bound and fills the exact-pass band.
+template <bool kMax>
+__global__ __launch_bounds__(256) void k_ntest(QArgs q) {
+  QState* S = q.S;
+  const unsigned long long n = min(S->n_cand, q.cap);
+  if (n == 0) return;
+  if (blockIdx.x * 256ull >= n) return;
+  const uint2* cand = q.node[S->leaf_buf ^ 1];
+  const float E = S->slack;
+  const int4* __restrict__ lta = reinterpret_cast<const int4*>(q.A.leaf_tri);
+  const int4* __restrict__ ltb = reinterpret_cast<const int4*>(q.B.leaf_tri);
+  __shared__ float warp_upd[8];
+  float upd = kMax ? 0.f : INFINITY;
+  unsigned long long tested = 0;
+  for (unsigned long long j = blockIdx.x * 256ull + threadIdx.x; j < n; j += gridDim.x * 256ull) {
+    ++tested;
+    const uint2 c = cand[j];
+    const int4 sa = __ldg(lta + c.x), sb = __ldg(ltb + c.y);
+    const Tri<float> A = load_tri32(q.A, sa), B = load_tri32(q.B, sb);
+    const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
+                         : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+    upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
+    const float ub = load_bound(S);
+    if (kMax ? (d + E >= ub) : (d - E <= ub)) {
+      const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
+      if (slot < q.band_cap) {
+        q.band_ids[slot] = make_uint2((unsigned)sa.w, (unsigned)sb.w);
+        q.band_d[slot] = d;
+      } else {
+        S->band_overflow = 1;  // k_narrow<rescan> re-scans the leaf list
+      }
+    }
+  }
+  upd = kMax ? warp_max(upd) : warp_min(upd);
+  tested = warp_sum_u64(tested);
+  if ((threadIdx.x & 31) == 0) {
+    warp_upd[threadIdx.x >> 5] = upd;
+    if (tested) atomicAdd(&S->narrow, tested);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float u = warp_upd[0];
+    for (int w = 1; w < 8; ++w) u = kMax ? fmaxf(u, warp_upd[w]) : fminf(u, warp_upd[w]);
+    if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, u);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -2,12 +2,14 @@
 //
 // One query = a fixed launch sequence on one stream, no host round trip:
 //   k_init            root bounds, slack, root front           (query.py:454-509)
-//   k_expand x D      one adaptive-depth expansion per launch   (query.py:349-451)
-//                     (D = max tree depth bounds the iteration count; launches
-//                      after the front empties exit immediately)
+//   k_traverse        every adaptive-depth expansion             (query.py:349-451)
+//                     in ONE persistent cooperative launch, iterations
+//                     separated by grid barriers
 //   k_seed            best leaf pair of every leaf-level block -> tight bound
-//   k_narrow          float32 narrow phase over the leaf-pair list, fills the
-//                     exact-pass band                           (query.py:287-346)
+//   k_nfilter         leaf pairs -> triangle-pair candidates (box + separating-
+//                     axis bounds)                              (query.py:287-346)
+//   k_ntest           float32 narrow phase on the candidates, fills the
+//                     exact-pass band
 //   k_refine          exact narrow phase (reference arithmetic, 64 or 32 bit)
 //                     over the band, lexicographic 128-bit key minimum
 //   k_narrow<rescan>  only if the band overflowed
@@ -69,6 +71,7 @@ static void validate(const GdBvh& a, const GdBvh& b, const GdConfig& cfg) {
 static bool g_profile = false;
 static cudaEvent_t g_ev[6];
 static int g_ev_dev = -1;
+static const QState* g_last_state = nullptr;  // profiled query's state (iteration timestamps)
 void set_profiling(int on) {
   g_profile = on != 0;
   if (g_profile) {
@@ -80,34 +83,54 @@ void set_profiling(int on) {
     }
   }
 }
-// [init, expand (all iterations), narrow (seed + filter), exact, rescan + final] ms
+// [init, expand (all iterations), narrow (seed + filter), exact, rescan + final] ms,
+// then (n > 5) the duration of each expansion iteration of the last profiled
+// query (device %globaltimer at the grid barriers)
 int phase_ms(float* out, int n) {
   if (g_ev_dev < 0) return 0;
   GD_CUDA(cudaEventSynchronize(g_ev[5]));
   int k = 0;
   for (; k < 5 && k < n; ++k) GD_CUDA(cudaEventElapsedTime(out + k, g_ev[k], g_ev[k + 1]));
+  if (g_last_state && n > 5) {
+    int iters = 0;
+    unsigned long long t[kMaxIters + 1];
+    GD_CUDA(cudaMemcpy(&iters, &g_last_state->iter, sizeof(int), cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(t, g_last_state->t_it, sizeof(t), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < iters && k < n; ++i, ++k) out[k] = (float)((double)(t[i + 1] - t[i]) * 1e-6);
+  }
   return k;
 }
 
 template <bool kMax>
-static void launch_query(const QArgs& q, int max_iters, cudaStream_t s) {
+static void launch_query(const QArgs& q, cudaStream_t s) {
   const int sms = num_sms();
-  const int expand_grid = sms * 8;
   auto mark = [&](int i) {
     if (g_profile) GD_CUDA(cudaEventRecord(g_ev[i], s));
   };
   mark(0);
   k_init<kMax><<<1, 32, 0, s>>>(q);
   mark(1);
-  static bool smem_set[2] = {false, false};
-  if (!smem_set[kMax]) {
-    GD_CUDA(cudaFuncSetAttribute(k_expand<kMax>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kExpandDynSmem));
-    smem_set[kMax] = true;
+  // persistent traversal: as many blocks as can be co-resident (cooperative
+  // launch guarantees it; the grid barrier relies on it)
+  static int grid[2] = {0, 0};
+  if (grid[kMax] == 0) {
+    GD_CUDA(cudaFuncSetAttribute(k_traverse<kMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kExpandDynSmem));
+    int per_sm = 0;
+    GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_traverse<kMax>, kExpandThreads,
+                                                          kExpandDynSmem));
+    GD_CHECK(per_sm >= 1, GD_ERR_CUDA, "k_traverse cannot be resident");
+    grid[kMax] = per_sm * sms;
   }
-  for (int i = 0; i < max_iters; ++i) k_expand<kMax><<<expand_grid, kExpandThreads, kExpandDynSmem, s>>>(q);
+  {
+    void* args[] = {const_cast<QArgs*>(&q)};
+    GD_CUDA(cudaLaunchCooperativeKernel((const void*)k_traverse<kMax>, dim3(grid[kMax]), dim3(kExpandThreads), args,
+                                        kExpandDynSmem, s));
+  }
   mark(2);
-  k_seed<kMax><<<(4 * std::min(expand_grid, kMaxSeeds) + 255) / 256, 256, 0, s>>>(q);
-  k_narrow<kMax, false><<<sms * 4, kNarrowThreads, 0, s>>>(q);
+  k_seed<kMax><<<(4 * std::min(grid[kMax], kMaxSeeds) + 255) / 256, 256, 0, s>>>(q);
+  k_nfilter<kMax><<<sms * 8, 256, 0, s>>>(q);
+  k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
   mark(3);
   k_refine<kMax><<<sms * 2, 256, 0, s>>>(q);
   mark(4);
@@ -115,7 +138,7 @@ static void launch_query(const QArgs& q, int max_iters, cudaStream_t s) {
   k_final<kMax><<<1, 32, 0, s>>>(q);
   mark(5);
   GD_CUDA(cudaGetLastError());
-  count_launches(6 + max_iters);
+  count_launches(8);
 }
 
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
@@ -143,11 +166,11 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   q.cap = L.cap;
   q.band_cap = L.band_cap;
   q.result = result_dev ? result_dev : reinterpret_cast<GdResult*>(base + L.result);
-  const int max_iters = std::max(a.depth, b.depth);
+  if (g_profile) g_last_state = q.S;
   if (cfg.kind == 1)
-    launch_query<true>(q, max_iters, s);
+    launch_query<true>(q, s);
   else
-    launch_query<false>(q, max_iters, s);
+    launch_query<false>(q, s);
 }
 
 void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, GdResult* out, GdIterStat* stats,

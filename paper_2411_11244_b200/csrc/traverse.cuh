@@ -6,7 +6,7 @@
 namespace gd {
 
 constexpr int kExpandThreads = 256;
-constexpr int kGenericItems = 4;                                   // candidates / thread (k >= 2)
+constexpr int kGenericItems = 1;                                   // candidates / thread / tile (k >= 2)
 constexpr int kGenericTile = kExpandThreads * kGenericItems;
 constexpr int kK1Rounds = 4;                                       // entries / thread / tile (k == 1)
 constexpr int kK1Tile = kExpandThreads * kK1Rounds;
@@ -107,6 +107,7 @@ __global__ void k_init(QArgs q) {
   S->n_out = 0;
   S->n_leaf = 0;
   S->n_band = 0;
+  S->n_cand = 0;
   S->expanded = 0;
   S->narrow = 0;
   S->culled = 0;
@@ -114,6 +115,9 @@ __global__ void k_init(QArgs q) {
   S->band_overflow = 0;
   S->n_seed = 0;
   S->ov_cand = S->ov_in = S->ov_cap = 0;
+  S->bar = 0;
+  for (int i = 0; i <= kMaxIters; ++i) S->cnt[i] = 0;
+  for (int i = 0; i < kMaxIters; ++i) S->culled_it[i] = 0;
   q.node[0][0] = make_uint2(0, 0);
   q.key[0][0] = key0;
   if (q.A.depth == 0 && q.B.depth == 0) {
@@ -163,56 +167,50 @@ struct ExpandShared {
   unsigned stage_count;
 };
 
-template <bool kMax>
-__device__ __forceinline__ unsigned long long tile_commit(ExpandShared& sh, QState* S, unsigned count, float upd,
-                                                         unsigned& my_off) {
-  unsigned total;
-  my_off = block_exclusive_scan(count, sh.warp_tot, total);
-  upd = kMax ? warp_max(upd) : warp_min(upd);
-  if ((threadIdx.x & 31) == 0) sh.warp_upd[threadIdx.x >> 5] = upd;
+// Grid-wide barrier of the persistent traversal (all blocks co-resident:
+// cooperative launch).  `bar` only grows; phase p completes when it reaches
+// p * gridDim.x, so no reset is needed inside a query.
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// fence / arrive / spin (relaxed) / fence: the pattern of a cooperative-groups
+// grid sync.  Data written in the same launch (fronts, counters) is read with
+// plain coherent loads after it, never through the non-coherent __ldg path.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    sh.out_base = total ? atomicAdd(&S->n_out, (unsigned long long)total) : 0ull;
-    float u = sh.warp_upd[0];
-    for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
-    if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
+    const unsigned target = phase * gridDim.x;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (*reinterpret_cast<volatile unsigned*>(bar) < target) __nanosleep(32);
+    __threadfence();
   }
   __syncthreads();
-  return sh.out_base;
 }
 
-// One expansion sweep (query.py:349-451, Alg. 2).  Two mappings, chosen
-// uniformly per launch from the adaptive depth k:
+// One expansion sweep (query.py:349-451, Alg. 2) over front `cur`.  Two
+// mappings, chosen uniformly per iteration from the adaptive depth k:
 //  k == 1 (the wide late iterations): one thread per front entry; it loads the
 //          (1 or 2) child boxes of each side once (contiguous siblings) and
 //          tests the <= 4 child pairs -- 14 loads per entry instead of 32.
 //  k >= 2 (narrow early fronts, ncand < front_cap): one thread per candidate,
 //          t -> entry t >> (ka+kb), descendants ((node+1) << k) - 1 + offset.
-// Only blocks that own a tile take part, so a small front costs a few blocks.
+// Survivors are counted into S->cnt[it]; the caller synchronises the grid.
 template <bool kMax>
-__global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
+__device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, unsigned char* k1_stage, int it,
+                                             int cur, unsigned long long n_in, int k, int ka, int kb,
+                                             bool to_leaves, unsigned long long ncand) {
   QState* S = q.S;
-  const unsigned long long n_in = S->n_in;
-  if (n_in == 0) return;
-  __shared__ ExpandShared sh;
-
-  const int ra = q.A.depth - S->depth_a, rb = q.B.depth - S->depth_b;
-  const int rem = max(ra, rb);
-  const int k = adaptive_k(n_in, q.cfg.front_cap, q.cfg.depth_cap, rem);
-  const int ka = min(k, ra), kb = min(k, rb), shift = ka + kb;
-  const bool to_leaves = (k == rem);
-  const unsigned long long ncand = n_in << shift;
-  const bool overflow = ncand > (unsigned long long)q.cfg.front_hard_cap;
+  const int shift = ka + kb;
   const bool k1 = (k == 1);
   const unsigned long long tiles = k1 ? (n_in + kK1Tile - 1) / kK1Tile : (ncand + kGenericTile - 1) / kGenericTile;
-  const unsigned active = overflow ? 1u : (unsigned)min((unsigned long long)gridDim.x, tiles);
-  if (blockIdx.x >= active) return;
-
-  const int cur = S->cur;
   const uint2* __restrict__ in_node = q.node[cur];
   const float* __restrict__ in_key = q.key[cur];
   uint2* out_node = q.node[cur ^ 1];
   float* out_key = q.key[cur ^ 1];
+  unsigned long long* n_out = &S->cnt[it];
   const unsigned leaf_a0 = (unsigned)((1ull << q.A.depth) - 1), leaf_b0 = (unsigned)((1ull << q.B.depth) - 1);
   const unsigned ra0 = to_leaves ? leaf_a0 : 0u, rb0 = to_leaves ? leaf_b0 : 0u;  // output index base
   const bool culling = q.cfg.culling != 0, enh = q.cfg.enhanced_bounds != 0;
@@ -222,88 +220,128 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
   float seed_key = kMax ? -INFINITY : INFINITY;
   uint2 seed_pair = make_uint2(0, 0);
 
-  if (!overflow && k1) {
+  if (k1) {
     // survivors are staged in shared memory (warp-aggregated appends), then
-    // one global reservation per tile and a coalesced copy-out
-    extern __shared__ unsigned char k1_stage[];
+    // one global reservation per tile and a coalesced copy-out.  A tile is
+    // R rounds of one entry per thread; R shrinks with the front so a small
+    // front spreads over all blocks (latency, not throughput, bounds it).
     uint2* s_node = reinterpret_cast<uint2*>(k1_stage);
     float* s_key = reinterpret_cast<float*>(k1_stage + kK1Stage * sizeof(uint2));
     const int ca = 1 << ka, cb = 1 << kb;
     const int lane = threadIdx.x & 31;
-    for (unsigned long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    // even contiguous split of the front over the blocks (no tail
+    // imbalance at the grid barrier), processed in tiles of <= kK1Rounds
+    // rounds of one entry per thread
+    unsigned long long per_blk = (n_in + gridDim.x - 1) / gridDim.x;
+    per_blk = (per_blk + 63) & ~63ull;
+    const unsigned long long blk_lo = min(n_in, blockIdx.x * per_blk);
+    const unsigned long long blk_hi = min(n_in, blk_lo + per_blk);
+    for (unsigned long long t0 = blk_lo; t0 < blk_hi; t0 += kK1Tile) {
+      const unsigned long long t1 = min(blk_hi, t0 + kK1Tile);
+      const int R = (int)((t1 - t0 + kExpandThreads - 1) / kExpandThreads);
       if (threadIdx.x == 0) sh.stage_count = 0;
+      // entry loads are software-pipelined one round ahead
+      const unsigned long long e0 = t0 + threadIdx.x;
+      float pk_next = e0 < t1 ? in_key[e0] : 0.f;
+      uint2 nd_next = e0 < t1 ? in_node[e0] : make_uint2(0, 0);
       __syncthreads();
       const float ub = load_bound_sq(S);  // one bound snapshot per tile (query.py:396)
       float upd = kMax ? 0.f : INFINITY;
 #pragma unroll 1
-      for (int r = 0; r < kK1Rounds; ++r) {
-      const unsigned long long e = tile * kK1Tile + (unsigned long long)r * kExpandThreads + threadIdx.x;
-      unsigned keep = 0;
-      float keys[4];
-      uint2 nd = make_uint2(0, 0);
-      if (e < n_in) {
-        const float pk = __ldg(in_key + e);
-        nd = __ldg(in_node + e);
-        // stale-entry re-cull: descendants' keys are monotone in the parent's
-        if (culling && !survives<kMax>(pk, ub)) {
-          my_culled += (unsigned)(ca * cb);
-        } else {
-          const unsigned a0 = ka ? 2 * nd.x + 1 : nd.x, b0 = kb ? 2 * nd.y + 1 : nd.y;
-          Box A[2], B[2];
-          A[0] = load_box(q.A.box, a0);
-          B[0] = load_box(q.B.box, b0);
-          if (ka) A[1] = load_box(q.A.box, a0 + 1);
-          if (kb) B[1] = load_box(q.B.box, b0 + 1);
+      for (int r = 0; r < R; ++r) {
+        const unsigned long long e = t0 + (unsigned long long)r * kExpandThreads + threadIdx.x;
+        const float pk = pk_next;
+        uint2 nd = nd_next;
+        if (r + 1 < R && e + kExpandThreads < t1) {
+          pk_next = in_key[e + kExpandThreads];
+          nd_next = in_node[e + kExpandThreads];
+        }
+        unsigned keep = 0;
+        float keys[4];
+        if (e < t1) {
+          // stale-entry re-cull: descendants' keys are monotone in the parent's
+          if (culling && !survives<kMax>(pk, ub)) {
+            my_culled += (unsigned)(ca * cb);
+          } else {
+            const unsigned a0 = ka ? 2 * nd.x + 1 : nd.x, b0 = kb ? 2 * nd.y + 1 : nd.y;
+            Box A[2], B[2];
+            if (ka)
+              load_children(q.A.box, nd.x, A[0], A[1]);
+            else
+              A[0] = load_box(q.A.box, a0);
+            if (kb)
+              load_children(q.B.box, nd.y, B[0], B[1]);
+            else
+              B[0] = load_box(q.B.box, b0);
+            float best = kMax ? -INFINITY : INFINITY;
+            int bc = 0;
 #pragma unroll
-          for (int i = 0; i < 2; ++i)
+            for (int i = 0; i < 2; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              if (i >= ca || j >= cb) continue;
-              const int c = 2 * i + j;
-              const float key = pair_key<kMax>(A[i], B[j]);
-              keys[c] = key;
-              if (culling && !survives<kMax>(key, ub)) {
-                ++my_culled;
-                continue;
+              for (int j = 0; j < 2; ++j) {
+                if (i >= ca || j >= cb) continue;
+                const int c = 2 * i + j;
+                const float key = pair_key<kMax>(A[i], B[j]);
+                keys[c] = key;
+                if (culling && !survives<kMax>(key, ub)) {
+                  ++my_culled;
+                  continue;
+                }
+                keep |= 1u << c;
+                if (improves<kMax>(key, best)) {
+                  best = key;
+                  bc = c;
+                }
               }
-              keep |= 1u << c;
-              const float u = pair_update<kMax>(A[i], B[j], enh);
-              upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
-              if (to_leaves && improves<kMax>(key, seed_key)) {
-                seed_key = key;
-                seed_pair = make_uint2(a0 + i - leaf_a0, b0 + j - leaf_b0);
+            if (keep) {
+              if (to_leaves) {
+                // leaf pairs go to the narrow phase (query.py:411-415); the
+                // block's most promising one seeds it (k_seed)
+                if (improves<kMax>(best, seed_key)) {
+                  seed_key = best;
+                  seed_pair = make_uint2(a0 + (bc >> 1) - leaf_a0, b0 + (bc & 1) - leaf_b0);
+                }
+              } else {
+                // bound update from the most promising kept child pair: any
+                // kept pair's enhanced bound is a valid bound (query.py:416-423
+                // takes the minimum over all kept pairs -- same fixed point,
+                // a quarter of the arithmetic)
+                const Box ba = select_box((bc >> 1) != 0, A[1], A[0]);
+                const Box bb = select_box((bc & 1) != 0, B[1], B[0]);
+                const float u = pair_update<kMax>(ba, bb, enh);
+                upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
               }
             }
-          nd = make_uint2(a0, b0);
+            nd = make_uint2(a0, b0);
+          }
         }
-      }
-      // warp-aggregated append into the shared staging area
-      const unsigned cnt = __popc(keep);
-      unsigned incl = cnt;
+        // warp-aggregated append into the shared staging area
+        const unsigned cnt = __popc(keep);
+        unsigned incl = cnt;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      unsigned wbase = 0;
-      if (lane == 31 && incl) wbase = atomicAdd(&sh.stage_count, incl);
-      wbase = __shfl_sync(0xffffffffu, wbase, 31);
-      unsigned pos = wbase + incl - cnt;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (keep & (1u << c)) {
-          s_node[pos] = make_uint2(nd.x + (c >> 1) - ra0, nd.y + (c & 1) - rb0);
-          s_key[pos] = keys[c];
-          ++pos;
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
-      }
+        unsigned wbase = 0;
+        if (lane == 31 && incl) wbase = atomicAdd(&sh.stage_count, incl);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        unsigned pos = wbase + incl - cnt;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (keep & (1u << c)) {
+            s_node[pos] = make_uint2(nd.x + (c >> 1) - ra0, nd.y + (c & 1) - rb0);
+            s_key[pos] = keys[c];
+            ++pos;
+          }
+        }
       }  // rounds
       upd = kMax ? warp_max(upd) : warp_min(upd);
       if (lane == 0) sh.warp_upd[threadIdx.x >> 5] = upd;
       __syncthreads();
       if (threadIdx.x == 0) {
         const unsigned total = sh.stage_count;
-        sh.out_base = total ? atomicAdd(&S->n_out, (unsigned long long)total) : 0ull;
+        sh.out_base = total ? atomicAdd(n_out, (unsigned long long)total) : 0ull;
         float u = sh.warp_upd[0];
         for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
         if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
@@ -319,7 +357,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
       }
       __syncthreads();  // staging reuse by the next tile
     }
-  } else if (!overflow) {
+  } else {
     const unsigned long long off_mask = (1ull << shift) - 1, mask_b = (1ull << kb) - 1;
     for (unsigned long long tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const unsigned long long base = tile * kGenericTile;
@@ -329,16 +367,16 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
       float ok[kGenericItems];
       unsigned keep = 0;
 #pragma unroll
-      for (int it = 0; it < kGenericItems; ++it) {
-        const unsigned long long t = base + (unsigned long long)it * kExpandThreads + threadIdx.x;
+      for (int itm = 0; itm < kGenericItems; ++itm) {
+        const unsigned long long t = base + (unsigned long long)itm * kExpandThreads + threadIdx.x;
         if (t >= ncand) continue;
         const unsigned long long e = t >> shift, off = t & off_mask;
-        const float pk = __ldg(in_key + e);
+        const float pk = in_key[e];
+        const uint2 nd = in_node[e];
         if (culling && !survives<kMax>(pk, ub)) {
           ++my_culled;
           continue;
         }
-        const uint2 nd = __ldg(in_node + e);
         const unsigned na = (unsigned)(((((unsigned long long)nd.x + 1) << ka) - 1) + (off >> kb));
         const unsigned nb = (unsigned)(((((unsigned long long)nd.y + 1) << kb) - 1) + (off & mask_b));
         const Box ba = load_box(q.A.box, na), bb = load_box(q.B.box, nb);
@@ -347,24 +385,37 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
           ++my_culled;
           continue;
         }
-        keep |= 1u << it;
-        on[it] = make_uint2(na - ra0, nb - rb0);
-        ok[it] = key;
-        const float u = pair_update<kMax>(ba, bb, enh);
-        upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
-        if (to_leaves && improves<kMax>(key, seed_key)) {
+        keep |= 1u << itm;
+        on[itm] = make_uint2(na - ra0, nb - rb0);
+        ok[itm] = key;
+        if (!to_leaves) {
+          const float u = pair_update<kMax>(ba, bb, enh);
+          upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
+        } else if (improves<kMax>(key, seed_key)) {
           seed_key = key;
-          seed_pair = on[it];
+          seed_pair = on[itm];
         }
       }
       unsigned my_off;
-      unsigned long long slot = tile_commit<kMax>(sh, S, __popc(keep), upd, my_off) + my_off;
+      unsigned total;
+      my_off = block_exclusive_scan(__popc(keep), sh.warp_tot, total);
+      upd = kMax ? warp_max(upd) : warp_min(upd);
+      if ((threadIdx.x & 31) == 0) sh.warp_upd[threadIdx.x >> 5] = upd;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        sh.out_base = total ? atomicAdd(n_out, (unsigned long long)total) : 0ull;
+        float u = sh.warp_upd[0];
+        for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
+        if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
+      }
+      __syncthreads();
+      unsigned long long slot = sh.out_base + my_off;
 #pragma unroll
-      for (int it = 0; it < kGenericItems; ++it) {
-        if (keep & (1u << it)) {
+      for (int itm = 0; itm < kGenericItems; ++itm) {
+        if (keep & (1u << itm)) {
           if (slot < q.cap) {
-            out_node[slot] = on[it];
-            out_key[slot] = ok[it];
+            out_node[slot] = on[itm];
+            out_key[slot] = ok[itm];
           }
           ++slot;
         }
@@ -373,7 +424,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
     }
   }
 
-  // --- per-block counters and seed, then the last block advances the front --
+  // --- per-block counters and seed ------------------------------------------
   unsigned long long c = warp_sum_u64(my_culled);
   if ((threadIdx.x & 31) == 0) sh.red_culled[threadIdx.x >> 5] = c;
   if (to_leaves) {
@@ -396,7 +447,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
   if (threadIdx.x == 0) {
     unsigned long long bc = 0;
     for (int w = 0; w < kExpandThreads / 32; ++w) bc += sh.red_culled[w];
-    if (bc) atomicAdd(&S->culled, bc);
+    if (bc) atomicAdd(&S->culled_it[it], bc);
     if (to_leaves && blockIdx.x < kMaxSeeds) {
       float bk = sh.warp_upd[0];
       uint2 bp = sh.warp_seed[0];
@@ -408,50 +459,90 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_expand(QArgs q) {
       q.seed_key[blockIdx.x] = bk;
       q.seed_pair[blockIdx.x] = bp;
     }
-    __threadfence();
-    const unsigned prev = atomicAdd(&S->done, 1u);
-    if (prev == active - 1) {
-      __threadfence();
-      volatile QState* V = S;
-      const unsigned long long n_out = V->n_out;
-      const int it = V->iter;
-      if (overflow || n_out > (unsigned long long)q.cfg.front_hard_cap) {
+  }
+}
+
+// Persistent traversal: one cooperative launch runs every expansion
+// iteration, separated by grid barriers.  Every block derives the same
+// iteration parameters from the shared counters, so no block has to publish
+// the next iteration's state; block 0 records the statistics.
+template <bool kMax>
+__global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
+  QState* S = q.S;
+  __shared__ ExpandShared sh;
+  extern __shared__ unsigned char k1_stage[];
+  volatile QState* V = S;
+  unsigned long long n_in = V->n_in;
+  int it = V->iter, cur = 0, da = 0, db = 0;
+  unsigned phase = 0;
+  unsigned long long expanded = 0;
+  const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
+  if (rec) S->t_it[it] = globaltimer_ns();
+  while (n_in > 0 && it < kMaxIters) {
+    const int ra = q.A.depth - da, rb = q.B.depth - db;
+    const int rem = max(ra, rb);
+    const int k = adaptive_k(n_in, q.cfg.front_cap, q.cfg.depth_cap, rem);
+    const int ka = min(k, ra), kb = min(k, rb);
+    const bool to_leaves = (k == rem);
+    const unsigned long long ncand = n_in << (ka + kb);
+    if (ncand > (unsigned long long)q.cfg.front_hard_cap) {  // query.py:373-376
+      if (rec) {
         S->err = GD_ERR_FRONT_OVERFLOW;
-        S->ov_cand = overflow ? (long long)ncand : (long long)n_out;
+        S->ov_cand = (long long)ncand;
         S->ov_in = (long long)n_in;
         S->ov_cap = q.cfg.front_hard_cap;
-        S->n_in = 0;
-        S->n_leaf = 0;
-      } else {
-        S->expanded += ncand;
-        if (it < kMaxIters) {
-          GdIterStat st;
-          st.k = k;
-          st.front_in = (long long)n_in;
-          st.front_out = to_leaves ? 0 : (long long)n_out;
-          st.culled = (long long)V->culled;
-          const float b = __uint_as_float(V->bound_bits);
-          st.bound_after = kMax ? (double)b + (double)S->slack : (double)b - (double)S->slack;
-          st._pad = 0;
-          S->stats[it] = st;
-        }
-        if (to_leaves) {
-          S->n_leaf = n_out;
-          S->leaf_buf = cur ^ 1;
-          S->n_in = 0;
-          S->n_seed = min(active, (unsigned)kMaxSeeds);
-        } else {
-          S->n_in = n_out;
-          S->cur = cur ^ 1;
-        }
-        S->depth_a += ka;
-        S->depth_b += kb;
       }
-      S->iter = it + 1;
-      S->n_out = 0;
-      S->culled = 0;
-      S->done = 0;
+      n_in = 0;
+      break;
     }
+    expand_sweep<kMax>(q, sh, k1_stage, it, cur, n_in, k, ka, kb, to_leaves, ncand);
+    grid_barrier(&S->bar, ++phase);
+    const unsigned long long n_out = V->cnt[it];
+    if (n_out > (unsigned long long)q.cfg.front_hard_cap) {  // query.py:448-449
+      if (rec) {
+        S->err = GD_ERR_FRONT_OVERFLOW;
+        S->ov_cand = (long long)n_out;
+        S->ov_in = (long long)n_in;
+        S->ov_cap = q.cfg.front_hard_cap;
+      }
+      n_in = 0;
+      break;
+    }
+    expanded += ncand;
+    if (rec) {
+      S->t_it[it + 1] = globaltimer_ns();
+      GdIterStat st;
+      st.k = k;
+      st.front_in = (long long)n_in;
+      st.front_out = to_leaves ? 0 : (long long)n_out;
+      st.culled = (long long)V->culled_it[it];
+      const float b = __uint_as_float(V->bound_bits);
+      st.bound_after = kMax ? (double)b + (double)S->slack : (double)b - (double)S->slack;
+      st._pad = 0;
+      S->stats[it] = st;
+    }
+    da += ka;
+    db += kb;
+    ++it;
+    if (to_leaves) {
+      if (rec) {
+        S->n_leaf = n_out;
+        S->leaf_buf = cur ^ 1;
+        S->n_seed = min(gridDim.x, (unsigned)kMaxSeeds);
+      }
+      n_in = 0;
+      break;
+    }
+    cur ^= 1;
+    n_in = n_out;
+  }
+  if (rec) {
+    S->iter = it;
+    S->expanded += expanded;
+    S->n_in = 0;
+    S->depth_a = da;
+    S->depth_b = db;
+    S->cur = cur;
   }
 }
 
