@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 1
+#define GDIST_ABI_VERSION 2
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -64,17 +64,21 @@ typedef struct GdBvhSizes {
 /* Device-resident f12-BVH (bvh.py:184-239).  Storage is implicit BFS: node
  * i has children 2i+1, 2i+2; leaves are the last L nodes.  All arrays are
  * caller-allocated device memory:
- *   box        : (n_nodes + 1) * 6 float32 (minx,miny,minz,maxx,maxy,maxz);
- *                node i at slot i + 1 (slot 0 is padding, so each sibling
- *                pair starts 16-byte aligned); traversal boxes of the
- *                float32-rounded vertices
- *   leaf_tri   : m * 4 int32  {v0, v1, v2, triangle id} in leaf (Morton) order
- *   leaf_first : (L + 1) uint32, first leaf_tri slot of each leaf
- *   vtx32      : nv * 4 float32, transformed float32 vertices (refit output)  */
+ *   box      : (n_nodes + 1) * 6 float32 (minx,miny,minz,maxx,maxy,maxz);
+ *              node i at slot i + 1 (slot 0 is padding, so each sibling
+ *              pair starts 16-byte aligned); traversal boxes of the
+ *              float32-transformed vertices (refit output)
+ *   leaf_rec : L * 8 int32, one 32-byte record per leaf in leaf (Morton)
+ *              order: {a0, a1, a2, b0, b1, b2, tri0, tri1} = the vertex
+ *              indices of the leaf's two triangles and their ids; a
+ *              single-triangle leaf repeats triangle 0 and has tri1 = -1
+ *   vtx32    : nv * 4 float32, float32 copy of the mesh's BASE vertices
+ *              (gd_stage_vertices; gd_bvh_build stages them).  Refit and
+ *              queries apply the mesh's (R, t) on the fly, so only a change
+ *              of the base vertex buffer needs a new gd_stage_vertices. */
 typedef struct GdBvh {
   float* box;
-  int32_t* leaf_tri;
-  uint32_t* leaf_first;
+  int32_t* leaf_rec;
   float* vtx32;
   int64_t leaf_count;
   int64_t n_tris;
@@ -151,8 +155,13 @@ int gd_bvh_sizes(int64_t m, int64_t nv, GdBvhSizes* out);
 int gd_bvh_build(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspace_bytes,
                  int64_t* prim_order_host, int64_t* leaf_tris_host, void* stream);
 
+/* float32 copy of mesh->vtx (the base vertices, before mesh->rot/trans)
+ * into bvh->vtx32.  Needed once per base vertex buffer. Asynchronous. */
+int gd_stage_vertices(const GdMesh* mesh, GdBvh* bvh, void* stream);
+
 /* refit (bvh.py:292-306) with apply_transform (mesh.py:102-105) fused:
- * transform + f32 vertices, leaf boxes, bottom-up unions. Asynchronous. */
+ * leaf boxes of the transformed staged vertices, bottom-up unions.
+ * Asynchronous. */
 int gd_refit(const GdMesh* mesh, GdBvh* bvh, void* stream);
 
 /* Node boxes with the reference's dtype semantics (bvh.py:242-264):

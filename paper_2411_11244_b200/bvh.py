@@ -53,8 +53,9 @@ class Aabb:
 class F12Bvh:
     """Full binary AABB tree in implicit BFS storage (bvh.py:184-239).
 
-    Device state: `_box` ((n_nodes + 1) x 6 float32 traversal boxes, node i at slot i + 1), `_leaf_tri`
-    (m x int4 leaf-ordered slots), `_leaf_first` (L + 1), `_vtx32`.
+    Device state (include/gdist.h GdBvh): `_box` ((n_nodes + 1) x 6 float32
+    traversal boxes, node i at slot i + 1), `_leaf_rec` (L x 8 int32 leaf
+    records), `_vtx32` (float32 copy of the base vertices of `_staged`).
     Host state: `leaf_tris` (L, 2) int64, `prim_order` (m,) int64, `depth`.
     """
 
@@ -68,9 +69,10 @@ class F12Bvh:
         self._host_boxes = None
         if node_min is not None:
             self._host_boxes = (np.asarray(node_min), np.asarray(node_max))
-        self._box = self._leaf_tri = self._leaf_first = self._vtx32 = None
+        self._box = self._leaf_rec = self._vtx32 = None
         self._mesh = None            # mesh of the last device refit
-        self._layout_tris = None     # index buffer the leaf slots were built from
+        self._staged = None          # root mesh whose base vertices are in _vtx32
+        self._layout_tris = None     # index buffer the leaf records were built from
         self._export_cache = None
 
     # -- reference-compatible accessors ------------------------------------
@@ -147,17 +149,14 @@ class F12Bvh:
     def _alloc(self, nv: int):
         torch = _lib.torch()
         L = self.leaf_count
-        m = len(self.prim_order)
         self._box = _lib.empty(2 * L * 6, torch.float32)  # slot 0 = padding (gdist.h)
-        self._leaf_tri = _lib.empty(m * 4, torch.int32)
-        self._leaf_first = _lib.empty(L + 1, torch.int32)
+        self._leaf_rec = _lib.empty(L * 8, torch.int32)
         self._vtx32 = _lib.empty(max(nv, 1) * 4, torch.float32)
 
     def device_view(self) -> _lib.GdBvh:
         g = _lib.GdBvh()
         g.box = self._box.data_ptr()
-        g.leaf_tri = self._leaf_tri.data_ptr()
-        g.leaf_first = self._leaf_first.data_ptr()
+        g.leaf_rec = self._leaf_rec.data_ptr()
         g.vtx32 = self._vtx32.data_ptr()
         g.leaf_count = self.leaf_count
         g.n_tris = len(self.prim_order)
@@ -166,11 +165,10 @@ class F12Bvh:
         return g
 
     def _ensure_layout(self, mesh: TriangleMesh):
-        """Device leaf layout for a tree given as host arrays (the reference
+        """Device leaf records for a tree given as host arrays (the reference
         allows constructing F12Bvh directly, bvh.py:184-199)."""
         if self._box is not None:
             return
-        torch = _lib.torch()
         self._alloc(mesh.n_vertices)
         counts = 1 + (self.leaf_tris[:, 1] >= 0)
         first = np.zeros(self.leaf_count + 1, dtype=np.int64)
@@ -178,17 +176,33 @@ class F12Bvh:
         # leaf_tris must list Morton-order neighbours: slot order == prim_order
         if not np.array_equal(self.prim_order[first[:-1]], self.leaf_tris[:, 0]):
             raise ValueError("leaf_tris is not consistent with prim_order")
-        self._leaf_first.copy_(torch.from_numpy(first.astype(np.int32)))
-        self._write_slots(mesh)
+        self._write_records(mesh)
         self._layout_tris = mesh.triangles
 
-    def _write_slots(self, mesh: TriangleMesh):
-        """Leaf-ordered {v0, v1, v2, id} slots from mesh.triangles."""
-        order = self.prim_order
-        slots = np.empty((len(order), 4), dtype=np.int32)
-        slots[:, :3] = mesh.triangles[order]
-        slots[:, 3] = order
-        self._leaf_tri.copy_(_lib.torch().from_numpy(slots.reshape(-1)))
+    def _write_records(self, mesh: TriangleMesh):
+        """Leaf records {a0, a1, a2, b0, b1, b2, tri0, tri1} (gdist.h) from
+        leaf_tris and mesh.triangles; a single repeats triangle 0."""
+        t0 = self.leaf_tris[:, 0]
+        t1 = self.leaf_tris[:, 1]
+        tris = mesh.triangles
+        rec = np.empty((self.leaf_count, 8), dtype=np.int32)
+        rec[:, 0:3] = tris[t0]
+        rec[:, 3:6] = tris[np.where(t1 >= 0, t1, t0)]
+        rec[:, 6] = t0
+        rec[:, 7] = t1
+        self._leaf_rec.copy_(_lib.torch().from_numpy(rec.reshape(-1)))
+
+    def _stage(self, mesh: TriangleMesh):
+        """float32 copy of the mesh's base vertices (once per base buffer)."""
+        if self._staged is mesh._root:
+            return
+        if self._vtx32.numel() < max(mesh.n_vertices, 1) * 4:
+            self._vtx32 = _lib.empty(mesh.n_vertices * 4, _lib.torch().float32)
+        g = mesh.device_view()
+        v = self.device_view()
+        v.nv = mesh.n_vertices
+        _lib.check(_lib.lib().gd_stage_vertices(C.byref(g), C.byref(v), _lib.stream_ptr()), "stage_vertices")
+        self._staged = mesh._root
 
     def _device_refit(self, mesh: TriangleMesh):
         if mesh.n_triangles != len(self.prim_order):
@@ -200,10 +214,9 @@ class F12Bvh:
             # same triangle count but possibly another index buffer: the
             # reference refits from mesh.triangles (bvh.py:244), so re-lay
             if self._layout_tris is None or not np.array_equal(self._layout_tris, mesh.triangles):
-                self._write_slots(mesh)
+                self._write_records(mesh)
             self._layout_tris = mesh.triangles
-        if self._vtx32.numel() < max(mesh.n_vertices, 1) * 4:
-            self._vtx32 = _lib.empty(mesh.n_vertices * 4, _lib.torch().float32)
+        self._stage(mesh)
         self._mesh = mesh
         g = mesh.device_view()
         v = self.device_view()
@@ -276,6 +289,7 @@ def build_f12(mesh: TriangleMesh, dtype=np.float64) -> F12Bvh:
         "bvh_build",
     )
     bvh._mesh = src
+    bvh._staged = src._root
     bvh._layout_tris = src.triangles
     bvh.prim_order.setflags(write=False)
     bvh.leaf_tris.setflags(write=False)

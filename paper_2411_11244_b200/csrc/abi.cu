@@ -21,6 +21,7 @@ size_t build_workspace_size(int64_t m);
 void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t* prim_order_host,
                int64_t* leaf_tris_host, cudaStream_t s);
 void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s);
+void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s);
 void export_boxes(const GdMesh& m, const GdBvh& B, int precision, void* nmin, void* nmax, cudaStream_t s);
 void pair_greedy(const double* sa, int64_t n, uint8_t* is_left);
 size_t query_workspace_size(const GdConfig& cfg);
@@ -115,6 +116,13 @@ int gd_bvh_build(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspa
   return guarded([&] {
     GD_CHECK(mesh && bvh && prim_order_host && leaf_tris_host, GD_ERR_INVALID, "null argument");
     bvh_build(*mesh, *bvh, workspace, workspace_bytes, prim_order_host, leaf_tris_host, S(stream));
+  });
+}
+
+int gd_stage_vertices(const GdMesh* mesh, GdBvh* bvh, void* stream) {
+  return guarded([&] {
+    GD_CHECK(mesh && bvh, GD_ERR_INVALID, "null argument");
+    stage_vertices(*mesh, *bvh, S(stream));
   });
 }
 

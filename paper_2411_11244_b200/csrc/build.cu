@@ -6,8 +6,8 @@
 //   radix sort     stable (code, id) sort == np.lexsort((ids, codes))
 //   k_pair_sa      float64 surface area of Morton neighbours (bvh.py:117-120)
 //   pair_greedy    exact greedy on the host (pairing.cpp)
-//   k_leaf_tri     leaf-ordered {v0, v1, v2, id} slots
-// then refit() fills every box.
+//   k_leaf_rec     one 32-byte record per leaf (gdist.h)
+// then the vertices are staged and refit() fills every box.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -18,6 +18,7 @@
 namespace gd {
 
 void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s);
+void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s);
 void pair_greedy(const double* sa, int64_t n, uint8_t* is_left);
 
 // order-preserving map of a double onto an unsigned 64-bit key
@@ -115,17 +116,23 @@ __global__ __launch_bounds__(256) void k_pair_sa(GdMesh m, const int32_t* order,
   sa[i] = E::add(E::add(E::mul(e[0], e[1]), E::mul(e[1], e[2])), E::mul(e[2], e[0]));
 }
 
-__global__ __launch_bounds__(256) void k_leaf_tri(GdMesh m, const int32_t* order, int4* leaf_tri) {
-  const long long i = blockIdx.x * 256ll + threadIdx.x;
-  if (i >= m.m) return;
-  const int32_t t = order[i];
-  const int32_t* ix = m.tri + 3 * (long long)t;
-  leaf_tri[i] = make_int4(ix[0], ix[1], ix[2], t);
+// leaf records in Morton order (bvh.py:168-181): leaf l holds Morton ranks
+// first[l] .. first[l + 1] - 1 (one or two triangles)
+__global__ __launch_bounds__(256) void k_leaf_rec(GdMesh m, const int32_t* order, const uint32_t* first, long long L,
+                                                  int4* rec) {
+  const long long l = blockIdx.x * 256ll + threadIdx.x;
+  if (l >= L) return;
+  const uint32_t f = first[l], c = first[l + 1] - f;
+  const int32_t t0 = order[f], t1 = c > 1 ? order[f + 1] : -1;
+  const int32_t* i0 = m.tri + 3 * (long long)t0;
+  const int32_t* i1 = m.tri + 3 * (long long)(t1 >= 0 ? t1 : t0);
+  rec[2 * l] = make_int4(i0[0], i0[1], i0[2], i1[0]);
+  rec[2 * l + 1] = make_int4(i1[1], i1[2], t0, t1);
 }
 
 // ---------------------------------------------------------------------------
 struct BuildWs {
-  size_t lohi, codes_in, codes_out, ids_in, ids_out, sa, cub, total, cub_bytes;
+  size_t lohi, codes_in, codes_out, ids_in, ids_out, sa, first, cub, total, cub_bytes;
 };
 static size_t al(size_t x) { return (x + 255) / 256 * 256; }
 
@@ -148,6 +155,8 @@ static BuildWs build_layout(int64_t m) {
   o = al(o + m * sizeof(int32_t));
   w.sa = o;
   o = al(o + m * sizeof(double));
+  w.first = o;
+  o = al(o + (m + 1) * sizeof(uint32_t));
   w.cub = o;
   w.cub_bytes = cub_bytes;
   o = al(o + cub_bytes);
@@ -188,7 +197,6 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
   size_t cub_bytes = w.cub_bytes;
   GD_CUDA(cub::DeviceRadixSort::SortPairs(base + w.cub, cub_bytes, codes_in, codes_out, ids_in, ids_out, (int)m, 0,
                                           63, s));
-  k_leaf_tri<<<g, 256, 0, s>>>(mesh, ids_out, reinterpret_cast<int4*>(T.leaf_tri));
   GD_CUDA(cudaGetLastError());
 
   std::vector<int32_t> order(m);
@@ -221,7 +229,11 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
   GD_CHECK(rank == L, GD_ERR_INVALID, "internal: pairing produced a wrong leaf count");
   first[L] = (uint32_t)m;
   for (int64_t i = 0; i < m; ++i) prim_order_host[i] = order[i];
-  GD_CUDA(cudaMemcpyAsync(T.leaf_first, first.data(), (L + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  auto* first_d = reinterpret_cast<uint32_t*>(base + w.first);
+  GD_CUDA(cudaMemcpyAsync(first_d, first.data(), (L + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  k_leaf_rec<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(mesh, ids_out, first_d, L, reinterpret_cast<int4*>(T.leaf_rec));
+  GD_CUDA(cudaGetLastError());
+  stage_vertices(mesh, T, s);
   refit(mesh, T, s);
   GD_CUDA(cudaStreamSynchronize(s));
 }

@@ -95,15 +95,54 @@ __device__ __forceinline__ Box box_union(const Box& a, const Box& b) {
   return r;
 }
 
-// float32 triangle of a leaf slot: {v0, v1, v2, id} -> three vertices
-__device__ __forceinline__ Tri<float> load_tri32(const GdBvh& T, const int4& s) {
+// Rigid transform of a mesh in float32 (from GdMesh's float64 R, t).  Every
+// float32 vertex the traversal sees -- refit boxes, seed, narrow filter --
+// goes through xf_apply on the staged float32 base vertex, so the boxes
+// contain exactly the vertices the narrow phase tests.
+struct XfF32 {
+  float r[9], t[3];
+  int has;
+};
+__device__ __forceinline__ XfF32 xf32_of(const GdMesh& m) {
+  XfF32 x;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) x.r[i] = (float)m.rot[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) x.t[i] = (float)m.trans[i];
+  x.has = m.has_xf;
+  return x;
+}
+__device__ __forceinline__ V3<float> xf_apply(const XfF32& x, const float4 v) {
+  if (!x.has) return {v.x, v.y, v.z};
+  return {fmaf(x.r[0], v.x, fmaf(x.r[1], v.y, fmaf(x.r[2], v.z, x.t[0]))),
+          fmaf(x.r[3], v.x, fmaf(x.r[4], v.y, fmaf(x.r[5], v.z, x.t[1]))),
+          fmaf(x.r[6], v.x, fmaf(x.r[7], v.y, fmaf(x.r[8], v.z, x.t[2])))};
+}
+// float32 triangle from three vertex indices of the staged base vertices
+__device__ __forceinline__ Tri<float> tri32(const GdBvh& T, const XfF32& x, int i0, int i1, int i2) {
   const float4* v = reinterpret_cast<const float4*>(T.vtx32);
-  float4 a = __ldg(v + s.x), b = __ldg(v + s.y), c = __ldg(v + s.z);
+  const float4 a = __ldg(v + i0), b = __ldg(v + i1), c = __ldg(v + i2);
   Tri<float> t;
-  t.v[0] = {a.x, a.y, a.z};
-  t.v[1] = {b.x, b.y, b.z};
-  t.v[2] = {c.x, c.y, c.z};
+  t.v[0] = xf_apply(x, a);
+  t.v[1] = xf_apply(x, b);
+  t.v[2] = xf_apply(x, c);
   return t;
+}
+// leaf record (gdist.h): {a0,a1,a2, b0,b1,b2, tri0, tri1}; r0 = first int4
+struct LeafRec {
+  int4 r0, r1;
+  __device__ __forceinline__ int count() const { return r1.w >= 0 ? 2 : 1; }
+  __device__ __forceinline__ unsigned tri_id(int i) const { return (unsigned)(i ? r1.w : r1.z); }
+};
+__device__ __forceinline__ LeafRec load_leaf(const GdBvh& T, unsigned long long leaf) {
+  const int4* p = reinterpret_cast<const int4*>(T.leaf_rec) + 2 * leaf;
+  LeafRec r;
+  r.r0 = __ldg(p);
+  r.r1 = __ldg(p + 1);
+  return r;
+}
+__device__ __forceinline__ Tri<float> leaf_tri32(const GdBvh& T, const XfF32& x, const LeafRec& r, int i) {
+  return i ? tri32(T, x, r.r0.w, r.r1.x, r.r1.y) : tri32(T, x, r.r0.x, r.r0.y, r.r0.z);
 }
 
 __device__ __forceinline__ Box tri_box(const Tri<float>& t) {

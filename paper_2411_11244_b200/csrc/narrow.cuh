@@ -7,7 +7,6 @@
 
 namespace gd {
 
-constexpr int kNarrowThreads = 256;
 
 // exact narrow phase for one triangle pair -> 128-bit key (distance bits,
 // tri_a, tri_b): its minimum is the reference's lexicographic witness rule
@@ -60,146 +59,30 @@ __device__ __forceinline__ float axis_gap_sq(const Tri<float>& a, const Tri<floa
 }
 
 // ---------------------------------------------------------------------------
-// fast float32 narrow phase over the leaf-pair list: every leaf pair expands
-// to its 1..4 triangle pairs inside the block (block scan), a triangle-box
-// prefilter compacts the survivors, then the full test runs on dense lanes.
-template <bool kMax, bool kRescan>
-__global__ __launch_bounds__(kNarrowThreads) void k_narrow(QArgs q) {
-  QState* S = q.S;
-  const unsigned long long n = S->n_leaf;
-  if (n == 0) return;
-  // rescan pass: only when the band overflowed; re-filters every pair with
-  // the final bound and evaluates the survivors exactly
-  if (kRescan && *reinterpret_cast<volatile int*>(&S->band_overflow) == 0) return;
-  if (blockIdx.x * (unsigned long long)kNarrowThreads >= n) return;
-  __shared__ unsigned warp_tot[kNarrowThreads / 32];
-  __shared__ unsigned char owner[kNarrowThreads * 4];
-  __shared__ unsigned s_off[kNarrowThreads];
-  __shared__ uint2 s_first[kNarrowThreads];
-  __shared__ unsigned char s_cb[kNarrowThreads];
-  __shared__ float warp_upd[kNarrowThreads / 32];
-  __shared__ unsigned short work[kNarrowThreads * 4];
-  __shared__ unsigned n_work;
-  const int buf = S->leaf_buf;
-  const uint2* __restrict__ leaves = q.node[buf];
-  const float* __restrict__ keys = q.key[buf];
-  const float E = S->slack;
-  const bool culling = q.cfg.culling != 0;
-  unsigned long long my_pairs = 0;
-  const int4* __restrict__ lta = reinterpret_cast<const int4*>(q.A.leaf_tri);
-  const int4* __restrict__ ltb = reinterpret_cast<const int4*>(q.B.leaf_tri);
-
-  for (unsigned long long tile = blockIdx.x; tile * kNarrowThreads < n; tile += gridDim.x) {
-    const unsigned long long i = tile * kNarrowThreads + threadIdx.x;
-    const float ub = load_bound(S);
-    unsigned cnt = 0;
-    uint2 first = make_uint2(0, 0);
-    unsigned cb = 1;
-    if (i < n) {
-      const float pk = keys[i];  // squared leaf-pair key
-      if (!culling || survives<kMax>(pk, ub * ub)) {
-        const uint2 lp = leaves[i];
-        const unsigned fa = __ldg(q.A.leaf_first + lp.x), ca = __ldg(q.A.leaf_first + lp.x + 1) - fa;
-        const unsigned fb = __ldg(q.B.leaf_first + lp.y);
-        cb = __ldg(q.B.leaf_first + lp.y + 1) - fb;
-        first = make_uint2(fa, fb);
-        cnt = ca * cb;
-      }
-    }
-    unsigned total;
-    const unsigned off = block_exclusive_scan(cnt, warp_tot, total);
-    s_off[threadIdx.x] = off;
-    s_first[threadIdx.x] = first;
-    s_cb[threadIdx.x] = (unsigned char)cb;
-    for (unsigned j = 0; j < cnt; ++j) owner[off + j] = (unsigned char)threadIdx.x;
-    if (threadIdx.x == 0) n_work = 0;
-    __syncthreads();
-    // stage 1: triangle-box prefilter, survivors compacted into `work`
-    const float ub1 = load_bound_sq(S);
-    for (unsigned s = threadIdx.x; s < total; s += kNarrowThreads) {
-      const int o = owner[s];
-      const unsigned j = s - s_off[o];
-      const unsigned cbo = s_cb[o];
-      const uint2 f = s_first[o];
-      const int4 sa = __ldg(lta + f.x + j / cbo);
-      const int4 sb = __ldg(ltb + f.y + j % cbo);
-      const Tri<float> ta = load_tri32(q.A, sa), tb = load_tri32(q.B, sb);
-      bool keep = !culling || survives<kMax>(pair_key<kMax>(tri_box(ta), tri_box(tb)), ub1);
-      // min query: separating-axis lower bound along the centroid axis --
-      // near contact it is within a triangle's thickness of the distance,
-      // where the box bound loses a whole triangle extent
-      if (!kMax && culling && keep) keep = axis_gap_sq(ta, tb) <= ub1;
-      if (keep) work[atomicAdd(&n_work, 1u)] = (unsigned short)s;
-    }
-    __syncthreads();
-    const unsigned nw = n_work;
-    float upd = kMax ? 0.f : INFINITY;
-    // stage 2: full narrow phase on the compacted survivors
-    for (unsigned w = threadIdx.x; w < nw; w += kNarrowThreads) {
-      const unsigned s = work[w];
-      const int o = owner[s];
-      const unsigned j = s - s_off[o];
-      const unsigned cbo = s_cb[o];
-      const uint2 f = s_first[o];
-      const int4 sa = __ldg(lta + f.x + j / cbo);
-      const int4 sb = __ldg(ltb + f.y + j % cbo);
-      const Tri<float> A = load_tri32(q.A, sa), B = load_tri32(q.B, sb);
-      const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
-                           : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
-      upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
-      const bool cand = kMax ? (d + E >= ub) : (d - E <= ub);
-      if (cand) {
-        if (kRescan) {
-          atomic_min_key(&S->best, exact_key<kMax>(q, (unsigned)sa.w, (unsigned)sb.w));
-          atomicAdd(&S->band_eval, 1ull);
-        } else {
-          const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
-          if (slot < q.band_cap) {
-            q.band_ids[slot] = make_uint2((unsigned)sa.w, (unsigned)sb.w);
-            q.band_d[slot] = d;
-          } else {
-            S->band_overflow = 1;  // k_narrow<kMax, true> re-scans the leaf list
-          }
-        }
-      }
-    }
-    if (kRescan) {
-      __syncthreads();
-      continue;
-    }
-    my_pairs += nw;
-    upd = kMax ? warp_max(upd) : warp_min(upd);
-    if ((threadIdx.x & 31) == 0) warp_upd[threadIdx.x >> 5] = upd;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      float u = warp_upd[0];
-      for (int w = 1; w < kNarrowThreads / 32; ++w) u = kMax ? fmaxf(u, warp_upd[w]) : fminf(u, warp_upd[w]);
-      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, u);
-    }
-    __syncthreads();
-  }
-  if (!kRescan && threadIdx.x == 0 && my_pairs) atomicAdd(&S->narrow, my_pairs);
-}
-
-// ---------------------------------------------------------------------------
 // Narrow phase, stage 1 (k_nfilter): one thread per leaf pair.  Re-culls the
-// pair with the (seeded) bound, loads its 1..2 x 1..2 triangles once, and
-// keeps the triangle pairs whose box bound -- and, for min queries, the
-// centroid-axis separation bound -- can still beat the bound.  Survivors
-// (leaf-slot index pairs) are appended, warp-aggregated, to the idle front
-// buffer; stage 2 (k_ntest) runs the full test on that dense list.
-template <bool kMax>
+// pair with the (seeded) bound, loads its 1..2 x 1..2 triangles once (two
+// 32-byte leaf records + staged vertices), and keeps the triangle pairs whose
+// box bound -- and, for min queries, the centroid-axis separation bound --
+// can still beat the bound.
+//  * min, normal pass: survivors (leaf rank * 2 + triangle) pairs are
+//    appended, warp-aggregated, to the idle front buffer; k_ntest runs the
+//    full test on that dense list.
+//  * max: the exact test is 9 vertex pairs -- cheaper here, on the loaded
+//    triangles, than a candidate round trip.
+//  * kRescan (only after a band / candidate overflow): every survivor of the
+//    final bound is evaluated in the reference arithmetic right here.
+template <bool kMax, bool kRescan>
 __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   QState* S = q.S;
   const unsigned long long n = S->n_leaf;
   if (n == 0) return;
+  if (kRescan && *reinterpret_cast<volatile int*>(&S->band_overflow) == 0) return;
   const int buf = S->leaf_buf;
   const uint2* leaves = q.node[buf];
   const float* keys = q.key[buf];
   uint2* out = q.node[buf ^ 1];
   const bool culling = q.cfg.culling != 0;
-  const int4* __restrict__ lta = reinterpret_cast<const int4*>(q.A.leaf_tri);
-  const int4* __restrict__ ltb = reinterpret_cast<const int4*>(q.B.leaf_tri);
+  const XfF32 xa = xf32_of(q.ma), xb = xf32_of(q.mb);
   const int lane = threadIdx.x & 31;
   const float E = S->slack;
   float upd = 0.f;  // max query only
@@ -209,80 +92,84 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
     const unsigned long long i = base + threadIdx.x;
     const float ub = load_bound(S), ub2 = ub * ub;
     unsigned mask = 0;
-    unsigned fa = 0, fb = 0;
+    uint2 lp = make_uint2(0, 0);
     if (i < n && (!culling || survives<kMax>(keys[i], ub2))) {
-      const uint2 lp = leaves[i];
-      fa = __ldg(q.A.leaf_first + lp.x);
-      const unsigned ca = __ldg(q.A.leaf_first + lp.x + 1) - fa;
-      fb = __ldg(q.B.leaf_first + lp.y);
-      const unsigned cb = __ldg(q.B.leaf_first + lp.y + 1) - fb;
+      lp = leaves[i];
+      const LeafRec ra = load_leaf(q.A, lp.x), rb = load_leaf(q.B, lp.y);
+      const int ca = ra.count(), cb = rb.count();
       Tri<float> ta[2], tb[2];
-      ta[0] = load_tri32(q.A, __ldg(lta + fa));
-      tb[0] = load_tri32(q.B, __ldg(ltb + fb));
-      if (ca > 1) ta[1] = load_tri32(q.A, __ldg(lta + fa + 1));
-      if (cb > 1) tb[1] = load_tri32(q.B, __ldg(ltb + fb + 1));
+      ta[0] = leaf_tri32(q.A, xa, ra, 0);
+      tb[0] = leaf_tri32(q.B, xb, rb, 0);
+      if (ca > 1) ta[1] = leaf_tri32(q.A, xa, ra, 1);
+      if (cb > 1) tb[1] = leaf_tri32(q.B, xb, rb, 1);
 #pragma unroll
       for (int ia = 0; ia < 2; ++ia)
 #pragma unroll
         for (int ib = 0; ib < 2; ++ib) {
-          if (ia >= (int)ca || ib >= (int)cb) continue;
+          if (ia >= ca || ib >= cb) continue;
           bool keep = !culling || survives<kMax>(pair_key<kMax>(tri_box(ta[ia]), tri_box(tb[ib])), ub2);
           if (!kMax && culling && keep) keep = axis_gap_sq(ta[ia], tb[ib]) <= ub2;
-          if (kMax && keep) {
-            // max query: the exact test is 9 vertex pairs -- cheaper here, on
-            // the loaded triangles, than a candidate round trip
-            const float d = sqrtf(tri_tri_max_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr));
-            upd = fmaxf(upd, d);
+          if (!keep) continue;
+          if (kMax || kRescan) {
+            const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr))
+                                 : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr));
+            if (kMax) upd = fmaxf(upd, d);
             ++tested;
-            if (d + E >= ub) {
-              const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
-              if (slot < q.band_cap) {
-                q.band_ids[slot] = make_uint2((unsigned)__ldg(lta + fa + ia).w, (unsigned)__ldg(ltb + fb + ib).w);
-                q.band_d[slot] = d;
+            if (kMax ? (d + E >= ub) : (d - E <= ub)) {
+              if (kRescan) {
+                atomic_min_key(&S->best, exact_key<kMax>(q, ra.tri_id(ia), rb.tri_id(ib)));
               } else {
-                S->band_overflow = 1;
+                const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
+                if (slot < q.band_cap) {
+                  q.band_ids[slot] = make_uint2(ra.tri_id(ia), rb.tri_id(ib));
+                  q.band_d[slot] = d;
+                } else {
+                  S->band_overflow = 1;
+                }
               }
             }
-            keep = false;
+          } else {
+            mask |= 1u << (2 * ia + ib);
           }
-          if (keep) mask |= 1u << (2 * ia + ib);
         }
     }
-    // warp-aggregated append of up to 4 slot pairs per thread
-    const unsigned cnt = __popc(mask);
-    unsigned incl = cnt;
+    if (!kMax && !kRescan) {
+      // warp-aggregated append of up to 4 triangle pairs per thread
+      const unsigned cnt = __popc(mask);
+      unsigned incl = cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    unsigned long long wbase = 0;
-    if (lane == 31 && incl) wbase = atomicAdd(&S->n_cand, (unsigned long long)incl);
-    wbase = __shfl_sync(0xffffffffu, wbase, 31);
-    unsigned long long pos = wbase + incl - cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      unsigned long long wbase = 0;
+      if (lane == 31 && incl) wbase = atomicAdd(&S->n_cand, (unsigned long long)incl);
+      wbase = __shfl_sync(0xffffffffu, wbase, 31);
+      unsigned long long pos = wbase + incl - cnt;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (mask & (1u << c)) {
-        if (pos < q.cap)
-          out[pos] = make_uint2(fa + (c >> 1), fb + (c & 1));
-        else
-          S->band_overflow = 1;  // k_narrow<rescan> re-scans every leaf pair exactly
-        ++pos;
+      for (int c = 0; c < 4; ++c) {
+        if (mask & (1u << c)) {
+          if (pos < q.cap)
+            out[pos] = make_uint2(2 * lp.x + (c >> 1), 2 * lp.y + (c & 1));
+          else
+            S->band_overflow = 1;  // the rescan pass covers every leaf pair
+          ++pos;
+        }
       }
     }
   }
-  if (kMax) {
+  if (kMax && !kRescan) {
     upd = warp_max(upd);
+    if (lane == 0 && upd > 0.f) commit_bound<kMax>(S, upd);
+  }
+  if (!kRescan) {
     tested = warp_sum_u64(tested);
-    if (lane == 0) {
-      if (upd > 0.f) commit_bound<kMax>(S, upd);
-      if (tested) atomicAdd(&S->narrow, tested);
-    }
+    if (lane == 0 && tested) atomicAdd(&S->narrow, tested);
   }
 }
 
-// Narrow phase, stage 2 (k_ntest): the float32 triangle-pair test on the
-// dense candidate list; updates the bound and fills the exact-pass band.
+// Narrow phase, stage 2 (k_ntest, min queries): the float32 triangle-pair
+// test on the dense candidate list; updates the bound and fills the band.
 template <bool kMax>
 __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   QState* S = q.S;
@@ -291,16 +178,16 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   if (blockIdx.x * 256ull >= n) return;
   const uint2* cand = q.node[S->leaf_buf ^ 1];
   const float E = S->slack;
-  const int4* __restrict__ lta = reinterpret_cast<const int4*>(q.A.leaf_tri);
-  const int4* __restrict__ ltb = reinterpret_cast<const int4*>(q.B.leaf_tri);
+  const XfF32 xa = xf32_of(q.ma), xb = xf32_of(q.mb);
   __shared__ float warp_upd[8];
   float upd = kMax ? 0.f : INFINITY;
   unsigned long long tested = 0;
   for (unsigned long long j = blockIdx.x * 256ull + threadIdx.x; j < n; j += gridDim.x * 256ull) {
     ++tested;
     const uint2 c = cand[j];
-    const int4 sa = __ldg(lta + c.x), sb = __ldg(ltb + c.y);
-    const Tri<float> A = load_tri32(q.A, sa), B = load_tri32(q.B, sb);
+    const LeafRec ra = load_leaf(q.A, c.x >> 1), rb = load_leaf(q.B, c.y >> 1);
+    const int ia = c.x & 1, ib = c.y & 1;
+    const Tri<float> A = leaf_tri32(q.A, xa, ra, ia), B = leaf_tri32(q.B, xb, rb, ib);
     const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
                          : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
     upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
@@ -308,10 +195,10 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
     if (kMax ? (d + E >= ub) : (d - E <= ub)) {
       const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
       if (slot < q.band_cap) {
-        q.band_ids[slot] = make_uint2((unsigned)sa.w, (unsigned)sb.w);
+        q.band_ids[slot] = make_uint2(ra.tri_id(ia), rb.tri_id(ib));
         q.band_d[slot] = d;
       } else {
-        S->band_overflow = 1;  // k_narrow<rescan> re-scans the leaf list
+        S->band_overflow = 1;  // the rescan pass covers every leaf pair
       }
     }
   }

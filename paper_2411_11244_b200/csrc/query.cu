@@ -12,7 +12,7 @@
 //                     exact-pass band
 //   k_refine          exact narrow phase (reference arithmetic, 64 or 32 bit)
 //                     over the band, lexicographic 128-bit key minimum
-//   k_narrow<rescan>  only if the band overflowed
+//   k_nfilter<rescan> only if the band / candidate list overflowed
 //   k_final           witness points (one warp), result record
 // The bound is a float32 cell carrying a slack E:
 // culling is conservative, so every pair that can attain the reference's
@@ -63,7 +63,7 @@ static void validate(const GdBvh& a, const GdBvh& b, const GdConfig& cfg) {
   GD_CHECK(cfg.front_hard_cap >= 4, GD_ERR_CONFIG, "front_hard_cap must be >= 4");
   GD_CHECK(a.depth >= 0 && a.depth <= 31 && b.depth >= 0 && b.depth <= 31, GD_ERR_INVALID,
            "tree depth out of range");
-  GD_CHECK(a.box && b.box && a.leaf_tri && b.leaf_tri && a.leaf_first && b.leaf_first && a.vtx32 && b.vtx32,
+  GD_CHECK(a.box && b.box && a.leaf_rec && b.leaf_rec && a.vtx32 && b.vtx32,
            GD_ERR_INVALID, "BVH arrays must be allocated");
 }
 
@@ -129,16 +129,16 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
   }
   mark(2);
   k_seed<kMax><<<(4 * std::min(grid[kMax], kMaxSeeds) + 255) / 256, 256, 0, s>>>(q);
-  k_nfilter<kMax><<<sms * 8, 256, 0, s>>>(q);
-  k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
+  k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
+  if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
   mark(3);
   k_refine<kMax><<<sms * 2, 256, 0, s>>>(q);
   mark(4);
-  k_narrow<kMax, true><<<sms * 4, kNarrowThreads, 0, s>>>(q);
+  k_nfilter<kMax, true><<<sms * 8, 256, 0, s>>>(q);
   k_final<kMax><<<1, 32, 0, s>>>(q);
   mark(5);
   GD_CUDA(cudaGetLastError());
-  count_launches(8);
+  count_launches(kMax ? 7 : 8);
 }
 
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,

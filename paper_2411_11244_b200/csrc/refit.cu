@@ -1,9 +1,11 @@
 // refit.cu -- per-frame refit (bvh.py:242-306) fused with apply_transform
 // (mesh.py:102-105).
 //
-//   k_xform        float64 base vertex -> R v + t -> float32 vertex (16 B)
-//   k_leaf_up      leaf box = union of its 1..2 triangles, then the block
-//                  folds its 256-leaf subtree 8 levels up in shared memory
+//   k_stage        float64 base vertex -> float32 float4 (once per base buffer)
+//   k_leaf_up      one thread per leaf: its 32-byte record, six staged vertex
+//                  gathers, float32 transform, leaf box = union of its 1..2
+//                  triangles; then the block folds its 256-leaf subtree 8
+//                  levels up in shared memory
 //   k_level_up     the same fold for the remaining top levels
 // Every node box is written exactly once; no level is re-read from HBM
 // except the <= 1/256 subtree roots handed from one fold to the next.
@@ -16,14 +18,12 @@ namespace gd {
 
 constexpr int kFold = 256;  // nodes per block per fold (8 levels)
 
-__global__ __launch_bounds__(256) void k_xform(GdMesh m, float4* __restrict__ out) {
+__global__ __launch_bounds__(256) void k_stage(GdMesh m, float4* __restrict__ out) {
   const long long i = blockIdx.x * 256ll + threadIdx.x;
   if (i >= m.nv) return;
-  V3<double> v = mesh_vertex(m, i);
-  out[i] = make_float4((float)v.x, (float)v.y, (float)v.z, 0.f);
+  const double* p = m.vtx + 3 * i;
+  out[i] = make_float4((float)p[0], (float)p[1], (float)p[2], 0.f);
 }
-
-__device__ __forceinline__ Box tri_box32(const GdBvh& T, const int4& s) { return tri_box(load_tri32(T, s)); }
 
 // fold `levels` levels inside the block; sb holds blockDim.x boxes of level
 // `lv`, the block covering nodes [first_rank, first_rank + blockDim.x)
@@ -47,13 +47,13 @@ __device__ __forceinline__ void fold_up(float* box, Box* sb, Box mine, int lv, l
   }
 }
 
-__global__ __launch_bounds__(kFold) void k_leaf_up(GdBvh T, int levels) {
+__global__ __launch_bounds__(kFold) void k_leaf_up(GdBvh T, GdMesh m, int levels) {
   __shared__ Box sb[kFold];
   const long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // leaf rank (< L exactly)
-  const int4* lt = reinterpret_cast<const int4*>(T.leaf_tri);
-  const unsigned f0 = T.leaf_first[l], f1 = T.leaf_first[l + 1];
-  Box b = tri_box32(T, __ldg(lt + f0));
-  if (f1 - f0 == 2) b = box_union(b, tri_box32(T, __ldg(lt + f0 + 1)));
+  const XfF32 x = xf32_of(m);
+  const LeafRec r = load_leaf(T, l);
+  // both triangles unconditionally: a single-triangle leaf repeats triangle 0
+  const Box b = box_union(tri_box(leaf_tri32(T, x, r, 0)), tri_box(leaf_tri32(T, x, r, 1)));
   store_box(T.box, (T.leaf_count - 1) + l, b);
   fold_up(T.box, sb, b, T.depth, blockIdx.x * (long long)blockDim.x, levels);
 }
@@ -65,20 +65,22 @@ __global__ __launch_bounds__(kFold) void k_level_up(float* box, int lv, int leve
   fold_up(box, sb, b, lv, blockIdx.x * (long long)blockDim.x, levels);
 }
 
+void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
+  GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "mesh vertex count differs from the tree's");
+  if (m.nv > 0) k_stage<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, reinterpret_cast<float4*>(T.vtx32));
+  GD_CUDA(cudaGetLastError());
+}
+
 void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.m == T.n_tris, GD_ERR_TOPOLOGY,
            "refit mesh has " + std::to_string(m.m) + " triangles, tree was built over " + std::to_string(T.n_tris));
   GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "refit mesh vertex count differs from the build");
   long long launches = 0;
-  if (m.nv > 0) {
-    k_xform<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, reinterpret_cast<float4*>(T.vtx32));
-    ++launches;
-  }
   const long long L = T.leaf_count;
   int lv = T.depth;
   const int bs = (int)std::min<long long>(L, kFold);
   const int lev = std::min(lv, __builtin_ctz((unsigned)bs));
-  k_leaf_up<<<(unsigned)(L / bs), bs, 0, s>>>(T, lev);
+  k_leaf_up<<<(unsigned)(L / bs), bs, 0, s>>>(T, m, lev);
   ++launches;
   lv -= lev;
   while (lv > 0) {
@@ -100,22 +102,20 @@ template <typename T>
 __global__ void k_export_leaf(GdMesh m, GdBvh B, T* nmin, T* nmax) {
   const long long l = blockIdx.x * 256ll + threadIdx.x;
   if (l >= B.leaf_count) return;
-  const int4* lt = reinterpret_cast<const int4*>(B.leaf_tri);
-  const unsigned f0 = B.leaf_first[l], f1 = B.leaf_first[l + 1];
+  const int4* rec = reinterpret_cast<const int4*>(B.leaf_rec) + 2 * l;
+  const int4 r0 = rec[0], r1 = rec[1];
+  const int v[6] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y};
+  const int nvert = r1.w >= 0 ? 6 : 3;
   T lo[3], hi[3];
-  for (unsigned f = f0; f < f1; ++f) {
-    const int4 s = lt[f];
-    const int v[3] = {s.x, s.y, s.z};
-    for (int c = 0; c < 3; ++c) {
-      V3<double> p = mesh_vertex(m, v[c]);
-      T x[3] = {T(p.x), T(p.y), T(p.z)};
-      for (int k = 0; k < 3; ++k) {
-        if (f == f0 && c == 0) {
-          lo[k] = hi[k] = x[k];
-        } else {
-          lo[k] = x[k] < lo[k] ? x[k] : lo[k];
-          hi[k] = x[k] > hi[k] ? x[k] : hi[k];
-        }
+  for (int c = 0; c < nvert; ++c) {
+    V3<double> p = mesh_vertex(m, v[c]);
+    T x[3] = {T(p.x), T(p.y), T(p.z)};
+    for (int k = 0; k < 3; ++k) {
+      if (c == 0) {
+        lo[k] = hi[k] = x[k];
+      } else {
+        lo[k] = x[k] < lo[k] ? x[k] : lo[k];
+        hi[k] = x[k] > hi[k] ? x[k] : hi[k];
       }
     }
   }

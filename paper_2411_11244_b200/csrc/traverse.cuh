@@ -143,8 +143,8 @@ __global__ void k_init(QArgs q) {
     unsigned ta = (unsigned)q.cfg.warm_a, tb = (unsigned)q.cfg.warm_b;
     const int32_t* ia = q.ma.tri + 3 * (long long)ta;
     const int32_t* ib = q.mb.tri + 3 * (long long)tb;
-    Tri<float> a = load_tri32(q.A, make_int4(ia[0], ia[1], ia[2], 0));
-    Tri<float> b = load_tri32(q.B, make_int4(ib[0], ib[1], ib[2], 0));
+    Tri<float> a = tri32(q.A, xf32_of(q.ma), ia[0], ia[1], ia[2]);
+    Tri<float> b = tri32(q.B, xf32_of(q.mb), ib[0], ib[1], ib[2]);
     float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(a, b, nullptr, nullptr))
                    : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(a, b, nullptr, nullptr));
     commit_bound<kMax>(S, d);
@@ -567,18 +567,15 @@ __global__ __launch_bounds__(256) void k_seed(QArgs q) {
     const float key = q.seed_key[t >> 2];
     if (isfinite(key)) {
       const uint2 lp = q.seed_pair[t >> 2];
-      const unsigned ia = (t >> 1) & 1, ib = t & 1;
-      const unsigned fa = q.A.leaf_first[lp.x], ca = q.A.leaf_first[lp.x + 1] - fa;
-      const unsigned fb = q.B.leaf_first[lp.y], cb = q.B.leaf_first[lp.y + 1] - fb;
-      if (ia < ca && ib < cb) {
-        const int4 sa = reinterpret_cast<const int4*>(q.A.leaf_tri)[fa + ia];
-        const int4 sb = reinterpret_cast<const int4*>(q.B.leaf_tri)[fb + ib];
-        const Tri<float> A = load_tri32(q.A, sa), B = load_tri32(q.B, sb);
+      const int ia = (t >> 1) & 1, ib = t & 1;
+      const LeafRec ra = load_leaf(q.A, lp.x), rb = load_leaf(q.B, lp.y);
+      if (ia < ra.count() && ib < rb.count()) {
+        const Tri<float> A = leaf_tri32(q.A, xf32_of(q.ma), ra, ia), B = leaf_tri32(q.B, xf32_of(q.mb), rb, ib);
         d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
                  : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
         valid = true;
-        ta = (unsigned)sa.w;
-        tb = (unsigned)sb.w;
+        ta = ra.tri_id(ia);
+        tb = rb.tri_id(ib);
       }
     }
   }

@@ -28,18 +28,38 @@ def test_library_exports_header(md):
     for name in declared:
         assert hasattr(lib, name), name
     assert sorted(_lib.exported_symbols()) == declared
-    assert lib.gd_abi_version() == 1
+    assert lib.gd_abi_version() == 2
     assert b"sm_100a" in lib.gd_version()
 
 
-def test_struct_sizes_match_header():
-    """ctypes mirrors of the C structs have the C layout sizes."""
+def test_struct_sizes_match_header(tmp_path):
+    """ctypes mirrors of the C structs have the layout the C compiler gives
+    include/gdist.h (sizes and every field offset)."""
+    import shutil
+    import subprocess
+
     from paper_2411_11244_b200 import _lib
 
-    assert C.sizeof(_lib.GdMesh) == 8 + 8 + 8 + 8 + 72 + 24 + 8
-    assert C.sizeof(_lib.GdBvh) == 4 * 8 + 3 * 8 + 8
-    assert C.sizeof(_lib.GdConfig) == 4 + 4 + 8 + 4 * 4 + 8 * 4
-    assert C.sizeof(_lib.GdIterStat) == 3 * 8 + 8 + 8
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    structs = {"GdMesh": _lib.GdMesh, "GdBvhSizes": _lib.GdBvhSizes, "GdBvh": _lib.GdBvh, "GdConfig": _lib.GdConfig,
+               "GdResult": _lib.GdResult, "GdIterStat": _lib.GdIterStat}
+    lines = ["#include <stdio.h>", "#include <stddef.h>", '#include "gdist.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "sizes.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "sizes"
+    subprocess.run(["gcc", "-I", str(REPO / "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == C.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
 
 
 def test_no_device_fails_loudly(md):
