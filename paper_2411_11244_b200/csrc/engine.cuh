@@ -23,7 +23,6 @@ struct alignas(16) QState {
   long long ov_cand, ov_in, ov_cap;
   float slack;
   int band_overflow;
-  unsigned n_seed;                   // blocks that wrote a seed leaf pair
   unsigned bar;                      // grid-barrier arrivals (k_traverse)
   unsigned long long cnt[kMaxIters + 1];       // survivors written by iteration i
   unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
@@ -31,7 +30,6 @@ struct alignas(16) QState {
   unsigned long long t_it[kMaxIters + 1];      // %globaltimer at iteration boundaries
 };
 
-constexpr int kMaxSeeds = 8192;
 
 struct QArgs {
   GdMesh ma, mb;
@@ -42,8 +40,6 @@ struct QArgs {
   float* key[2];
   uint2* band_ids;
   float* band_d;
-  uint2* seed_pair;             // per expand block: its best leaf pair
-  float* seed_key;
   unsigned long long cap;       // front / leaf-list capacity (entries)
   unsigned long long band_cap;  // band capacity (entries)
   GdResult* result;             // device result record
@@ -96,7 +92,7 @@ __device__ __forceinline__ Box box_union(const Box& a, const Box& b) {
 }
 
 // Rigid transform of a mesh in float32 (from GdMesh's float64 R, t).  Every
-// float32 vertex the traversal sees -- refit boxes, seed, narrow filter --
+// float32 vertex the traversal sees -- refit boxes, narrow filter --
 // goes through xf_apply on the staged float32 base vertex, so the boxes
 // contain exactly the vertices the narrow phase tests.
 struct XfF32 {

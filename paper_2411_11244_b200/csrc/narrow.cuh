@@ -60,7 +60,7 @@ __device__ __forceinline__ float axis_gap_sq(const Tri<float>& a, const Tri<floa
 
 // ---------------------------------------------------------------------------
 // Narrow phase, stage 1 (k_nfilter): one thread per leaf pair.  Re-culls the
-// pair with the (seeded) bound, loads its 1..2 x 1..2 triangles once (two
+// pair with the final traversal bound, loads its 1..2 x 1..2 triangles once (two
 // 32-byte leaf records + staged vertices), and keeps the triangle pairs whose
 // box bound -- and, for min queries, the centroid-axis separation bound --
 // can still beat the bound.
@@ -221,41 +221,56 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
 // the answer (|d_fast - d_exact| <= E/2) are re-evaluated in the reference's
 // arithmetic; the 128-bit minimum is the answer and its witness.
 template <bool kMax>
+__device__ void finalize(const QArgs& q);
+
+template <bool kMax>
 __global__ __launch_bounds__(256) void k_refine(QArgs q) {
   QState* S = q.S;
   const unsigned long long n = min(S->n_band, q.band_cap);
-  if (blockIdx.x * 256ull >= n) return;
-  const float E = S->slack;
-  const float ub = load_bound(S);
   __shared__ Key128 wk[8];
-  Key128 best;
-  best.hi = ~0ull;
-  best.lo = ~0ull;
-  unsigned long long evals = 0;
-  for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
-    const float d = q.band_d[i];
-    if (kMax ? (d + E >= ub) : (d - E <= ub)) {
-      const uint2 ids = q.band_ids[i];
-      Key128 k = exact_key<kMax>(q, ids.x, ids.y);
-      if (key_less(k, best)) best = k;
-      ++evals;
+  __shared__ bool last;
+  if (blockIdx.x * 256ull < n) {
+    const float E = S->slack;
+    const float ub = load_bound(S);
+    Key128 best;
+    best.hi = ~0ull;
+    best.lo = ~0ull;
+    unsigned long long evals = 0;
+    for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
+      const float d = q.band_d[i];
+      if (kMax ? (d + E >= ub) : (d - E <= ub)) {
+        const uint2 ids = q.band_ids[i];
+        Key128 k = exact_key<kMax>(q, ids.x, ids.y);
+        if (key_less(k, best)) best = k;
+        ++evals;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      Key128 other = shfl_key(best, o);
+      if (key_less(other, best)) best = other;
+    }
+    evals = warp_sum_u64(evals);
+    if ((threadIdx.x & 31) == 0) {
+      wk[threadIdx.x >> 5] = best;
+      if (evals) atomicAdd(&S->band_eval, evals);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < 8; ++w)
+        if (key_less(wk[w], best)) best = wk[w];
+      if (best.hi != ~0ull) atomic_min_key(&S->best, best);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    Key128 other = shfl_key(best, o);
-    if (key_less(other, best)) best = other;
-  }
-  evals = warp_sum_u64(evals);
-  if ((threadIdx.x & 31) == 0) {
-    wk[threadIdx.x >> 5] = best;
-    if (evals) atomicAdd(&S->band_eval, evals);
+  // the last block to finish writes the witness and the result record
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&S->done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w)
-      if (key_less(wk[w], best)) best = wk[w];
-    if (best.hi != ~0ull) atomic_min_key(&S->best, best);
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    finalize<kMax>(q);
   }
 }
 
@@ -337,9 +352,11 @@ __device__ void warp_witness(const Tri<T>& a, const Tri<T>& b, V3<T>& P, V3<T>& 
 }
 
 template <bool kMax>
-__global__ void k_final(QArgs q) {
+__device__ void finalize(const QArgs& q) {
   QState* S = q.S;
-  const Key128 best = S->best;
+  Key128 best;
+  best.hi = reinterpret_cast<volatile unsigned long long*>(&S->best)[0];
+  best.lo = reinterpret_cast<volatile unsigned long long*>(&S->best)[1];
   const bool found = !(best.hi == ~0ull && best.lo == ~0ull);
   const unsigned ta = (unsigned)(best.lo >> 32), tb = (unsigned)(best.lo & 0xffffffffu);
   double pa[3] = {0, 0, 0}, pb[3] = {0, 0, 0};

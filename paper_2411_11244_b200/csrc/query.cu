@@ -1,19 +1,18 @@
 // query.cu -- host orchestration of a BVTT distance query (query.py:480-568).
 //
 // One query = a fixed launch sequence on one stream, no host round trip:
-//   k_init            root bounds, slack, root front           (query.py:454-509)
-//   k_traverse        every adaptive-depth expansion             (query.py:349-451)
-//                     in ONE persistent cooperative launch, iterations
-//                     separated by grid barriers
-//   k_seed            best leaf pair of every leaf-level block -> tight bound
+//   memset            grid-barrier counter
+//   k_traverse        ONE persistent cooperative launch: root bounds, slack,
+//                     root front (query.py:454-509), then every adaptive-depth
+//                     expansion (query.py:349-451) separated by grid barriers
 //   k_nfilter         leaf pairs -> triangle-pair candidates (box + separating-
 //                     axis bounds)                              (query.py:287-346)
-//   k_ntest           float32 narrow phase on the candidates, fills the
+//   k_ntest           float32 narrow phase on the candidates (min), fills the
 //                     exact-pass band
+//   k_nfilter<rescan> exits at once unless the band / candidate list overflowed
 //   k_refine          exact narrow phase (reference arithmetic, 64 or 32 bit)
-//                     over the band, lexicographic 128-bit key minimum
-//   k_nfilter<rescan> only if the band / candidate list overflowed
-//   k_final           witness points (one warp), result record
+//                     over the band, lexicographic 128-bit key minimum; its
+//                     last block writes the witness points and the result
 // The bound is a float32 cell carrying a slack E:
 // culling is conservative, so every pair that can attain the reference's
 // exact answer reaches the exact pass.
@@ -24,7 +23,7 @@
 namespace gd {
 
 struct WsLayout {
-  size_t state, node0, key0, node1, key1, band_ids, band_d, seed_pair, seed_key, result, total;
+  size_t state, node0, key0, node1, key1, band_ids, band_d, result, total;
   unsigned long long cap, band_cap;
 };
 
@@ -47,8 +46,6 @@ static WsLayout ws_layout(const GdConfig& cfg) {
   take(L.key1, L.cap * sizeof(float));
   take(L.band_ids, L.band_cap * sizeof(uint2));
   take(L.band_d, L.band_cap * sizeof(float));
-  take(L.seed_pair, kMaxSeeds * sizeof(uint2));
-  take(L.seed_key, kMaxSeeds * sizeof(float));
   L.total = o;
   return L;
 }
@@ -83,7 +80,7 @@ void set_profiling(int on) {
     }
   }
 }
-// [init, expand (all iterations), narrow (seed + filter), exact, rescan + final] ms,
+// [init, expand (all iterations), narrow (filter + test), exact + witness, -] ms,
 // then (n > 5) the duration of each expansion iteration of the last profiled
 // query (device %globaltimer at the grid barriers)
 int phase_ms(float* out, int n) {
@@ -108,7 +105,9 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
     if (g_profile) GD_CUDA(cudaEventRecord(g_ev[i], s));
   };
   mark(0);
-  k_init<kMax><<<1, 32, 0, s>>>(q);
+  // the grid-barrier counter must start at 0; everything else is initialised
+  // by k_traverse's prologue
+  GD_CUDA(cudaMemsetAsync(&q.S->bar, 0, sizeof(unsigned), s));
   mark(1);
   // persistent traversal: as many blocks as can be co-resident (cooperative
   // launch guarantees it; the grid barrier relies on it)
@@ -128,17 +127,15 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
                                         kExpandDynSmem, s));
   }
   mark(2);
-  k_seed<kMax><<<(4 * std::min(grid[kMax], kMaxSeeds) + 255) / 256, 256, 0, s>>>(q);
   k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
   if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
   mark(3);
-  k_refine<kMax><<<sms * 2, 256, 0, s>>>(q);
+  k_nfilter<kMax, true><<<sms * 8, 256, 0, s>>>(q);  // exits at once unless the band overflowed
+  k_refine<kMax><<<sms * 2, 256, 0, s>>>(q);          // + witness record in its last block
   mark(4);
-  k_nfilter<kMax, true><<<sms * 8, 256, 0, s>>>(q);
-  k_final<kMax><<<1, 32, 0, s>>>(q);
   mark(5);
   GD_CUDA(cudaGetLastError());
-  count_launches(kMax ? 7 : 8);
+  count_launches(kMax ? 4 : 5);
 }
 
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
@@ -161,8 +158,6 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   q.key[1] = reinterpret_cast<float*>(base + L.key1);
   q.band_ids = reinterpret_cast<uint2*>(base + L.band_ids);
   q.band_d = reinterpret_cast<float*>(base + L.band_d);
-  q.seed_pair = reinterpret_cast<uint2*>(base + L.seed_pair);
-  q.seed_key = reinterpret_cast<float*>(base + L.seed_key);
   q.cap = L.cap;
   q.band_cap = L.band_cap;
   q.result = result_dev ? result_dev : reinterpret_cast<GdResult*>(base + L.result);

@@ -79,10 +79,26 @@ __device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* w
   return off + x - v;
 }
 
-// ---------------------------------------------------------------------------
+// closest (min) / farthest (max) vertex pair of two triangles
 template <bool kMax>
-__global__ void k_init(QArgs q) {
-  if (threadIdx.x != 0) return;
+__device__ __forceinline__ float vertex_pair_bound(const Tri<float>& a, const Tri<float>& b) {
+  float best = kMax ? 0.f : INFINITY;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float dx = a.v[i].x - b.v[j].x, dy = a.v[i].y - b.v[j].y, dz = a.v[i].z - b.v[j].z;
+      const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+      best = kMax ? fmaxf(best, d2) : fminf(best, d2);
+    }
+  return sqrtf(best);
+}
+
+// ---------------------------------------------------------------------------
+// query prologue (one thread; k_traverse block 0 before its first barrier):
+// root key and bound, slack, root front, counters, warm_pair
+template <bool kMax>
+__device__ void init_query(const QArgs& q) {
   QState* S = q.S;
   Box ra = load_box(q.A.box, 0), rb = load_box(q.B.box, 0);
   float M = 0.f;
@@ -113,9 +129,7 @@ __global__ void k_init(QArgs q) {
   S->culled = 0;
   S->band_eval = 0;
   S->band_overflow = 0;
-  S->n_seed = 0;
   S->ov_cand = S->ov_in = S->ov_cap = 0;
-  S->bar = 0;
   for (int i = 0; i <= kMaxIters; ++i) S->cnt[i] = 0;
   for (int i = 0; i < kMaxIters; ++i) S->culled_it[i] = 0;
   q.node[0][0] = make_uint2(0, 0);
@@ -143,13 +157,13 @@ __global__ void k_init(QArgs q) {
     unsigned ta = (unsigned)q.cfg.warm_a, tb = (unsigned)q.cfg.warm_b;
     const int32_t* ia = q.ma.tri + 3 * (long long)ta;
     const int32_t* ib = q.mb.tri + 3 * (long long)tb;
+    // the pair always reaches the exact pass (band distance -inf / +inf);
+    // its vertex-pair distance is an achieved distance, hence a valid bound
     Tri<float> a = tri32(q.A, xf32_of(q.ma), ia[0], ia[1], ia[2]);
     Tri<float> b = tri32(q.B, xf32_of(q.mb), ib[0], ib[1], ib[2]);
-    float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(a, b, nullptr, nullptr))
-                   : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(a, b, nullptr, nullptr));
-    commit_bound<kMax>(S, d);
+    commit_bound<kMax>(S, vertex_pair_bound<kMax>(a, b));
     q.band_ids[0] = make_uint2(ta, tb);
-    q.band_d[0] = d;
+    q.band_d[0] = kMax ? INFINITY : -INFINITY;
     S->n_band = 1;
   }
 }
@@ -163,7 +177,6 @@ struct ExpandShared {
   unsigned long long out_base;
   float warp_upd[kExpandThreads / 32];
   unsigned long long red_culled[kExpandThreads / 32];
-  uint2 warp_seed[kExpandThreads / 32];
   unsigned stage_count;
 };
 
@@ -190,6 +203,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned phase) {
   __syncthreads();
 }
 
+
 // One expansion sweep (query.py:349-451, Alg. 2) over front `cur`.  Two
 // mappings, chosen uniformly per iteration from the adaptive depth k:
 //  k == 1 (the wide late iterations): one thread per front entry; it loads the
@@ -215,10 +229,6 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
   const unsigned ra0 = to_leaves ? leaf_a0 : 0u, rb0 = to_leaves ? leaf_b0 : 0u;  // output index base
   const bool culling = q.cfg.culling != 0, enh = q.cfg.enhanced_bounds != 0;
   unsigned long long my_culled = 0;
-  // leaf level: each block remembers its most promising leaf pair; k_seed
-  // evaluates these first so the narrow phase starts from a tight bound
-  float seed_key = kMax ? -INFINITY : INFINITY;
-  uint2 seed_pair = make_uint2(0, 0);
 
   if (k1) {
     // survivors are staged in shared memory (warp-aggregated appends), then
@@ -293,24 +303,16 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
                   bc = c;
                 }
               }
-            if (keep) {
-              if (to_leaves) {
-                // leaf pairs go to the narrow phase (query.py:411-415); the
-                // block's most promising one seeds it (k_seed)
-                if (improves<kMax>(best, seed_key)) {
-                  seed_key = best;
-                  seed_pair = make_uint2(a0 + (bc >> 1) - leaf_a0, b0 + (bc & 1) - leaf_b0);
-                }
-              } else {
-                // bound update from the most promising kept child pair: any
-                // kept pair's enhanced bound is a valid bound (query.py:416-423
-                // takes the minimum over all kept pairs -- same fixed point,
-                // a quarter of the arithmetic)
-                const Box ba = select_box((bc >> 1) != 0, A[1], A[0]);
-                const Box bb = select_box((bc & 1) != 0, B[1], B[0]);
-                const float u = pair_update<kMax>(ba, bb, enh);
-                upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
-              }
+            // leaf pairs go to the narrow phase and emit no bound
+            // (query.py:411-415); otherwise the bound is updated from the
+            // most promising kept child pair: any kept pair's enhanced bound
+            // is a valid bound (query.py:416-423 takes the minimum over all
+            // kept pairs -- same fixed point, a quarter of the arithmetic)
+            if (keep && !to_leaves) {
+              const Box ba = select_box((bc >> 1) != 0, A[1], A[0]);
+              const Box bb = select_box((bc & 1) != 0, B[1], B[0]);
+              const float u = pair_update<kMax>(ba, bb, enh);
+              upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
             }
             nd = make_uint2(a0, b0);
           }
@@ -391,9 +393,6 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
         if (!to_leaves) {
           const float u = pair_update<kMax>(ba, bb, enh);
           upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
-        } else if (improves<kMax>(key, seed_key)) {
-          seed_key = key;
-          seed_pair = on[itm];
         }
       }
       unsigned my_off;
@@ -424,41 +423,14 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
     }
   }
 
-  // --- per-block counters and seed ------------------------------------------
+  // --- per-block counters -----------------------------------------------------
   unsigned long long c = warp_sum_u64(my_culled);
   if ((threadIdx.x & 31) == 0) sh.red_culled[threadIdx.x >> 5] = c;
-  if (to_leaves) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float k2 = __shfl_xor_sync(0xffffffffu, seed_key, o);
-      const unsigned px = __shfl_xor_sync(0xffffffffu, seed_pair.x, o);
-      const unsigned py = __shfl_xor_sync(0xffffffffu, seed_pair.y, o);
-      if (improves<kMax>(k2, seed_key)) {
-        seed_key = k2;
-        seed_pair = make_uint2(px, py);
-      }
-    }
-    if ((threadIdx.x & 31) == 0) {
-      sh.warp_upd[threadIdx.x >> 5] = seed_key;
-      sh.warp_seed[threadIdx.x >> 5] = seed_pair;
-    }
-  }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long bc = 0;
     for (int w = 0; w < kExpandThreads / 32; ++w) bc += sh.red_culled[w];
     if (bc) atomicAdd(&S->culled_it[it], bc);
-    if (to_leaves && blockIdx.x < kMaxSeeds) {
-      float bk = sh.warp_upd[0];
-      uint2 bp = sh.warp_seed[0];
-      for (int w = 1; w < kExpandThreads / 32; ++w)
-        if (improves<kMax>(sh.warp_upd[w], bk)) {
-          bk = sh.warp_upd[w];
-          bp = sh.warp_seed[w];
-        }
-      q.seed_key[blockIdx.x] = bk;
-      q.seed_pair[blockIdx.x] = bp;
-    }
   }
 }
 
@@ -472,11 +444,13 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
   __shared__ ExpandShared sh;
   extern __shared__ unsigned char k1_stage[];
   volatile QState* V = S;
+  const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
+  if (rec) init_query<kMax>(q);  // S->bar was zeroed by the host (memset node)
+  unsigned phase = 0;
+  grid_barrier(&S->bar, ++phase);
   unsigned long long n_in = V->n_in;
   int it = V->iter, cur = 0, da = 0, db = 0;
-  unsigned phase = 0;
   unsigned long long expanded = 0;
-  const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
   if (rec) S->t_it[it] = globaltimer_ns();
   while (n_in > 0 && it < kMaxIters) {
     const int ra = q.A.depth - da, rb = q.B.depth - db;
@@ -528,7 +502,6 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
       if (rec) {
         S->n_leaf = n_out;
         S->leaf_buf = cur ^ 1;
-        S->n_seed = min(gridDim.x, (unsigned)kMaxSeeds);
       }
       n_in = 0;
       break;
@@ -543,61 +516,6 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
     S->depth_a = da;
     S->depth_b = db;
     S->cur = cur;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// seed pass: the best leaf pair of every leaf-level expand block goes through
-// the narrow phase first, so the main pass culls against a bound close to the
-// answer (the reference gets this from its sequential batches, query.py:396,
-// 411-415).  Seed pairs that can still be the answer also join the band.
-template <bool kMax>
-__global__ __launch_bounds__(256) void k_seed(QArgs q) {
-  QState* S = q.S;
-  const unsigned ns = S->n_seed;
-  if (ns == 0 || S->n_leaf == 0) return;
-  if (blockIdx.x * 256 >= 4 * ns) return;
-  __shared__ float warp_upd[8];
-  const unsigned t = blockIdx.x * 256 + threadIdx.x;
-  const float E = S->slack;
-  float d = kMax ? 0.f : INFINITY;
-  bool valid = false;
-  unsigned ta = 0, tb = 0;
-  if (t < 4 * ns) {
-    const float key = q.seed_key[t >> 2];
-    if (isfinite(key)) {
-      const uint2 lp = q.seed_pair[t >> 2];
-      const int ia = (t >> 1) & 1, ib = t & 1;
-      const LeafRec ra = load_leaf(q.A, lp.x), rb = load_leaf(q.B, lp.y);
-      if (ia < ra.count() && ib < rb.count()) {
-        const Tri<float> A = leaf_tri32(q.A, xf32_of(q.ma), ra, ia), B = leaf_tri32(q.B, xf32_of(q.mb), rb, ib);
-        d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
-                 : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
-        valid = true;
-        ta = ra.tri_id(ia);
-        tb = rb.tri_id(ib);
-      }
-    }
-  }
-  float u = kMax ? warp_max(d) : warp_min(d);
-  if ((threadIdx.x & 31) == 0) warp_upd[threadIdx.x >> 5] = u;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) u = kMax ? fmaxf(u, warp_upd[w]) : fminf(u, warp_upd[w]);
-    if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, u);
-  }
-  __syncthreads();
-  if (valid) {
-    const float ub = load_bound(S);
-    if (kMax ? (d + E >= ub) : (d - E <= ub)) {
-      const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
-      if (slot < q.band_cap) {
-        q.band_ids[slot] = make_uint2(ta, tb);
-        q.band_d[slot] = d;
-      } else {
-        S->band_overflow = 1;
-      }
-    }
   }
 }
 
