@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 2
+#define GDIST_ABI_VERSION 4
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -69,17 +69,35 @@ typedef struct GdBvhSizes {
  *              pair starts 16-byte aligned); traversal boxes of the
  *              float32-transformed vertices (refit output)
  *   leaf_rec : L * 8 int32, one 32-byte record per leaf in leaf (Morton)
- *              order: {a0, a1, a2, b0, b1, b2, tri0, tri1} = the vertex
- *              indices of the leaf's two triangles and their ids; a
- *              single-triangle leaf repeats triangle 0 and has tri1 = -1
- *   vtx32    : nv * 4 float32, float32 copy of the mesh's BASE vertices
- *              (gd_stage_vertices; gd_bvh_build stages them).  Refit and
- *              queries apply the mesh's (R, t) on the fly, so only a change
- *              of the base vertex buffer needs a new gd_stage_vertices. */
+ *              order: {a0, a1, a2, b0, b1, b2, tri0, tri1} = the staged
+ *              vertex slots (vtx32 indices) of the leaf's two triangles and
+ *              their triangle ids; a single-triangle leaf repeats triangle 0
+ *              and has tri1 = -1
+ *   vtx32    : nv * 4 float32, float32 copy of the mesh's BASE vertices in
+ *              first-use order of the leaf records (gd_stage_vertices;
+ *              gd_bvh_build / gd_bvh_layout stage them).  Refit and queries
+ *              apply the mesh's (R, t) on the fly, so only a change of the
+ *              base vertex buffer needs a new gd_stage_vertices.
+ *   vmap     : nv int32, vtx32 slot of each mesh vertex
+ *   leaf_vtx : 3 * L float4 = three planes of L float4 holding the first
+ *              four distinct staged vertices of every leaf (x0 y0 z0 x1 |
+ *              y1 z1 x2 y2 | z2 x3 y3 z3; repeats pad leaves with fewer):
+ *              the refit streams these instead of gathering vertices
+ *   leaf_x   : 2 * ceil(L / 32) + 1 + 2 * (L >> 16) + 4 uint32: per 32
+ *              leaves a mask of the leaves with 5-6 distinct vertices, then
+ *              per 32 leaves the rank of their first extra record, then a
+ *              counter, then the refit's subtree arrival counters
+ *   leaf_xvtx: 2 * L float4 (capacity): the 5th and 6th distinct vertex
+ *              (repeated when only five) of each masked leaf, by rank
+ * leaf_vtx, leaf_x and leaf_xvtx are written by gd_stage_vertices. */
 typedef struct GdBvh {
   float* box;
   int32_t* leaf_rec;
   float* vtx32;
+  int32_t* vmap;
+  float* leaf_vtx;
+  uint32_t* leaf_x;
+  float* leaf_xvtx;
   int64_t leaf_count;
   int64_t n_tris;
   int64_t nv;
@@ -155,8 +173,15 @@ int gd_bvh_sizes(int64_t m, int64_t nv, GdBvhSizes* out);
 int gd_bvh_build(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspace_bytes,
                  int64_t* prim_order_host, int64_t* leaf_tris_host, void* stream);
 
+/* Leaf records written with ORIGINAL mesh vertex indices (a tree laid out
+ * on the host) -> first-use staged numbering: writes vmap, remaps the records
+ * in place, stages the vertices.  workspace: GdBvhSizes.build_workspace_bytes.
+ * gd_bvh_build does this itself.  Asynchronous. */
+int gd_bvh_layout(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspace_bytes, void* stream);
+
 /* float32 copy of mesh->vtx (the base vertices, before mesh->rot/trans)
- * into bvh->vtx32.  Needed once per base vertex buffer. Asynchronous. */
+ * into bvh->vtx32 at the slots of bvh->vmap.  Needed once per base vertex
+ * buffer. Asynchronous. */
 int gd_stage_vertices(const GdMesh* mesh, GdBvh* bvh, void* stream);
 
 /* refit (bvh.py:292-306) with apply_transform (mesh.py:102-105) fused:

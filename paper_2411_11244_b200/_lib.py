@@ -56,6 +56,10 @@ class GdBvh(C.Structure):
         ("box", C.c_void_p),
         ("leaf_rec", C.c_void_p),
         ("vtx32", C.c_void_p),
+        ("vmap", C.c_void_p),
+        ("leaf_vtx", C.c_void_p),
+        ("leaf_x", C.c_void_p),
+        ("leaf_xvtx", C.c_void_p),
         ("leaf_count", C.c_int64),
         ("n_tris", C.c_int64),
         ("nv", C.c_int64),
@@ -121,6 +125,7 @@ _SIGNATURES = {
     "gd_query_phase_ms": (C.c_int, [C.POINTER(C.c_float), C.c_int]),
     "gd_bvh_sizes": (C.c_int, [C.c_int64, C.c_int64, C.POINTER(GdBvhSizes)]),
     "gd_bvh_build": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P, C.c_size_t, P, P, P]),
+    "gd_bvh_layout": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P, C.c_size_t, P]),
     "gd_stage_vertices": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P]),
     "gd_refit": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P]),
     "gd_export_boxes": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), C.c_int, P, P, P]),

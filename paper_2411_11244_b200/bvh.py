@@ -55,7 +55,9 @@ class F12Bvh:
 
     Device state (include/gdist.h GdBvh): `_box` ((n_nodes + 1) x 6 float32
     traversal boxes, node i at slot i + 1), `_leaf_rec` (L x 8 int32 leaf
-    records), `_vtx32` (float32 copy of the base vertices of `_staged`).
+    records), `_vtx32` (float32 copy of the base vertices of `_staged`, in
+    first-use order), `_vmap` (staged slot of each mesh vertex), and the
+    refit's streamed per-leaf vertex sets `_leaf_vtx`, `_leaf_x`, `_leaf_xvtx`.
     Host state: `leaf_tris` (L, 2) int64, `prim_order` (m,) int64, `depth`.
     """
 
@@ -69,7 +71,8 @@ class F12Bvh:
         self._host_boxes = None
         if node_min is not None:
             self._host_boxes = (np.asarray(node_min), np.asarray(node_max))
-        self._box = self._leaf_rec = self._vtx32 = None
+        self._box = self._leaf_rec = self._vtx32 = self._vmap = None
+        self._leaf_vtx = self._leaf_x = self._leaf_xvtx = None
         self._mesh = None            # mesh of the last device refit
         self._staged = None          # root mesh whose base vertices are in _vtx32
         self._layout_tris = None     # index buffer the leaf records were built from
@@ -152,12 +155,21 @@ class F12Bvh:
         self._box = _lib.empty(2 * L * 6, torch.float32)  # slot 0 = padding (gdist.h)
         self._leaf_rec = _lib.empty(L * 8, torch.int32)
         self._vtx32 = _lib.empty(max(nv, 1) * 4, torch.float32)
+        self._vmap = _lib.empty(max(nv, 1), torch.int32)
+        self._leaf_vtx = _lib.empty(3 * L * 4, torch.float32)
+        self._leaf_x = _lib.torch().zeros(2 * ((L + 31) // 32) + 1 + 2 * (L >> 16) + 4, dtype=torch.int32,
+                                          device=_lib.device())
+        self._leaf_xvtx = _lib.empty(2 * L * 4, torch.float32)
 
     def device_view(self) -> _lib.GdBvh:
         g = _lib.GdBvh()
         g.box = self._box.data_ptr()
         g.leaf_rec = self._leaf_rec.data_ptr()
         g.vtx32 = self._vtx32.data_ptr()
+        g.vmap = self._vmap.data_ptr()
+        g.leaf_vtx = self._leaf_vtx.data_ptr()
+        g.leaf_x = self._leaf_x.data_ptr()
+        g.leaf_xvtx = self._leaf_xvtx.data_ptr()
         g.leaf_count = self.leaf_count
         g.n_tris = len(self.prim_order)
         g.nv = self._vtx32.numel() // 4 if self._mesh is None else self._mesh.n_vertices
@@ -181,7 +193,9 @@ class F12Bvh:
 
     def _write_records(self, mesh: TriangleMesh):
         """Leaf records {a0, a1, a2, b0, b1, b2, tri0, tri1} (gdist.h) from
-        leaf_tris and mesh.triangles; a single repeats triangle 0."""
+        leaf_tris and mesh.triangles (a single repeats triangle 0), then the
+        device layout pass renumbers their vertices by first use and stages
+        the mesh's vertices (gd_bvh_layout)."""
         t0 = self.leaf_tris[:, 0]
         t1 = self.leaf_tris[:, 1]
         tris = mesh.triangles
@@ -190,14 +204,30 @@ class F12Bvh:
         rec[:, 3:6] = tris[np.where(t1 >= 0, t1, t0)]
         rec[:, 6] = t0
         rec[:, 7] = t1
-        self._leaf_rec.copy_(_lib.torch().from_numpy(rec.reshape(-1)))
+        torch = _lib.torch()
+        nv = max(mesh.n_vertices, 1)
+        if self._vtx32.numel() != nv * 4:
+            self._vtx32 = _lib.empty(nv * 4, torch.float32)
+            self._vmap = _lib.empty(nv, torch.int32)
+        self._leaf_rec.copy_(torch.from_numpy(rec.reshape(-1)))
+        L = _lib.lib()
+        sizes = _lib.GdBvhSizes()
+        _lib.check(L.gd_bvh_sizes(len(self.prim_order), mesh.n_vertices, C.byref(sizes)), "bvh_sizes")
+        ws = _lib.empty(max(int(sizes.build_workspace_bytes), 1), torch.uint8)
+        g = mesh.device_view()
+        v = self.device_view()
+        v.nv = mesh.n_vertices
+        _lib.check(L.gd_bvh_layout(C.byref(g), C.byref(v), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "bvh_layout")
+        self._staged = mesh._root
 
     def _stage(self, mesh: TriangleMesh):
         """float32 copy of the mesh's base vertices (once per base buffer)."""
         if self._staged is mesh._root:
             return
-        if self._vtx32.numel() < max(mesh.n_vertices, 1) * 4:
-            self._vtx32 = _lib.empty(mesh.n_vertices * 4, _lib.torch().float32)
+        if self._vtx32.numel() != max(mesh.n_vertices, 1) * 4:
+            # another vertex count: the staged numbering must be rebuilt
+            self._write_records(mesh)
+            return
         g = mesh.device_view()
         v = self.device_view()
         v.nv = mesh.n_vertices

@@ -17,7 +17,8 @@ void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_rel
 void set_profiling(int on);
 int phase_ms(float* out, int n);
 
-size_t build_workspace_size(int64_t m);
+size_t build_workspace_size(int64_t m, int64_t nv);
+void bvh_layout(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, cudaStream_t s);
 void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t* prim_order_host,
                int64_t* leaf_tris_host, cudaStream_t s);
 void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s);
@@ -107,7 +108,7 @@ int gd_bvh_sizes(int64_t m, int64_t nv, GdBvhSizes* out) {
     out->n_nodes = 2 * L - 1;
     out->depth = d;
     out->_pad = 0;
-    out->build_workspace_bytes = build_workspace_size(m);
+    out->build_workspace_bytes = build_workspace_size(m, nv);
   });
 }
 
@@ -116,6 +117,13 @@ int gd_bvh_build(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspa
   return guarded([&] {
     GD_CHECK(mesh && bvh && prim_order_host && leaf_tris_host, GD_ERR_INVALID, "null argument");
     bvh_build(*mesh, *bvh, workspace, workspace_bytes, prim_order_host, leaf_tris_host, S(stream));
+  });
+}
+
+int gd_bvh_layout(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    GD_CHECK(mesh && bvh, GD_ERR_INVALID, "null argument");
+    bvh_layout(*mesh, *bvh, workspace, workspace_bytes, S(stream));
   });
 }
 

@@ -7,7 +7,9 @@
 //   k_pair_sa      float64 surface area of Morton neighbours (bvh.py:117-120)
 //   pair_greedy    exact greedy on the host (pairing.cpp)
 //   k_leaf_rec     one 32-byte record per leaf (gdist.h)
-// then the vertices are staged and refit() fills every box.
+//   bvh_layout     staged-vertex numbering by first use in leaf order
+//                  (k_first_use + radix sort + k_rec_remap), staging
+// then refit() fills every box.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -131,11 +133,86 @@ __global__ __launch_bounds__(256) void k_leaf_rec(GdMesh m, const int32_t* order
 }
 
 // ---------------------------------------------------------------------------
+// vertex layout: staged vertices are renumbered by first use in leaf-record
+// order, so the leaves of one warp gather from a few contiguous lines
+__global__ __launch_bounds__(256) void k_first_init(uint32_t* first, int32_t* ids, long long nv) {
+  const long long v = blockIdx.x * 256ll + threadIdx.x;
+  if (v >= nv) return;
+  first[v] = 0xFFFFFFFFu;
+  ids[v] = (int32_t)v;
+}
+__global__ __launch_bounds__(256) void k_first_use(const int32_t* rec, long long L, uint32_t* first) {
+  const long long l = blockIdx.x * 256ll + threadIdx.x;
+  if (l >= L) return;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) atomicMin(first + rec[8 * l + c], (uint32_t)(6 * l + c));
+}
+__global__ __launch_bounds__(256) void k_vmap(const int32_t* sorted_ids, long long nv, int32_t* vmap) {
+  const long long r = blockIdx.x * 256ll + threadIdx.x;
+  if (r < nv) vmap[sorted_ids[r]] = (int32_t)r;
+}
+__global__ __launch_bounds__(256) void k_rec_remap(int32_t* rec, long long L, const int32_t* vmap) {
+  const long long l = blockIdx.x * 256ll + threadIdx.x;
+  if (l >= L) return;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) rec[8 * l + c] = vmap[rec[8 * l + c]];
+}
+
+struct LayoutWs {
+  size_t first, first_out, ids, ids_out, cub, cub_bytes, total;
+};
+static size_t al(size_t x) { return (x + 255) / 256 * 256; }
+static LayoutWs layout_ws(int64_t nv) {
+  LayoutWs w;
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(nv, 1), 0, 32);
+  size_t o = 0;
+  w.first = o;
+  o = al(o + nv * sizeof(uint32_t));
+  w.first_out = o;
+  o = al(o + nv * sizeof(uint32_t));
+  w.ids = o;
+  o = al(o + nv * sizeof(int32_t));
+  w.ids_out = o;
+  o = al(o + nv * sizeof(int32_t));
+  w.cub = o;
+  w.cub_bytes = cub_bytes;
+  o = al(o + cub_bytes);
+  w.total = o;
+  return w;
+}
+
+void bvh_layout(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int64_t nv = mesh.nv, L = T.leaf_count;
+  GD_CHECK(nv == T.nv && nv < (1ll << 31) && T.vmap, GD_ERR_INVALID, "GdBvh does not match the mesh");
+  LayoutWs w = layout_ws(nv);
+  GD_CHECK(ws != nullptr && ws_bytes >= w.total, GD_ERR_WORKSPACE,
+           "layout workspace too small: need " + std::to_string(w.total) + " bytes");
+  char* base = static_cast<char*>(ws);
+  auto* first = reinterpret_cast<uint32_t*>(base + w.first);
+  auto* first_out = reinterpret_cast<uint32_t*>(base + w.first_out);
+  auto* ids = reinterpret_cast<int32_t*>(base + w.ids);
+  auto* ids_out = reinterpret_cast<int32_t*>(base + w.ids_out);
+  const unsigned gv = (unsigned)((nv + 255) / 256), gl = (unsigned)((L + 255) / 256);
+  if (nv > 0) {
+    k_first_init<<<gv, 256, 0, s>>>(first, ids, nv);
+    k_first_use<<<gl, 256, 0, s>>>(T.leaf_rec, L, first);
+    size_t cub_bytes = w.cub_bytes;
+    GD_CUDA(cub::DeviceRadixSort::SortPairs(base + w.cub, cub_bytes, first, first_out, ids, ids_out, (int)nv, 0, 32,
+                                            s));
+    k_vmap<<<gv, 256, 0, s>>>(ids_out, nv, T.vmap);
+    k_rec_remap<<<gl, 256, 0, s>>>(T.leaf_rec, L, T.vmap);
+  }
+  GD_CUDA(cudaGetLastError());
+  stage_vertices(mesh, T, s);
+}
+
+size_t layout_workspace_size(int64_t nv) { return layout_ws(nv).total; }
+
 struct BuildWs {
   size_t lohi, codes_in, codes_out, ids_in, ids_out, sa, first, cub, total, cub_bytes;
 };
-static size_t al(size_t x) { return (x + 255) / 256 * 256; }
-
 static BuildWs build_layout(int64_t m) {
   BuildWs w;
   size_t cub_bytes = 0;
@@ -164,7 +241,9 @@ static BuildWs build_layout(int64_t m) {
   return w;
 }
 
-size_t build_workspace_size(int64_t m) { return build_layout(m).total; }
+size_t build_workspace_size(int64_t m, int64_t nv) {
+  return std::max(build_layout(m).total, layout_ws(nv).total);
+}
 
 void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t* prim_order_host,
                int64_t* leaf_tris_host, cudaStream_t s) {
@@ -180,7 +259,7 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
   GD_CHECK(T.leaf_count == L && T.depth == depth && T.n_tris == m && T.nv == mesh.nv, GD_ERR_INVALID,
            "GdBvh sizes do not match the mesh (use gd_bvh_sizes)");
   BuildWs w = build_layout(m);
-  GD_CHECK(ws != nullptr && ws_bytes >= w.total, GD_ERR_WORKSPACE,
+  GD_CHECK(ws != nullptr && ws_bytes >= build_workspace_size(m, mesh.nv), GD_ERR_WORKSPACE,
            "build workspace too small: need " + std::to_string(w.total) + " bytes");
   char* base = static_cast<char*>(ws);
   auto* lohi = reinterpret_cast<unsigned long long*>(base + w.lohi);
@@ -233,7 +312,7 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
   GD_CUDA(cudaMemcpyAsync(first_d, first.data(), (L + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
   k_leaf_rec<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(mesh, ids_out, first_d, L, reinterpret_cast<int4*>(T.leaf_rec));
   GD_CUDA(cudaGetLastError());
-  stage_vertices(mesh, T, s);
+  bvh_layout(mesh, T, ws, ws_bytes, s);  // reuses the workspace (stream-ordered)
   refit(mesh, T, s);
   GD_CUDA(cudaStreamSynchronize(s));
 }

@@ -7,6 +7,23 @@ namespace gd {
 
 constexpr int kMaxIters = 64;
 
+// Rigid transform of a mesh in float32 (from GdMesh's float64 R, t).  Every
+// float32 vertex the traversal sees -- refit boxes, narrow filter --
+// goes through xf_apply on the staged float32 base vertex, so the boxes
+// contain exactly the vertices the narrow phase tests.
+struct XfF32 {
+  float r[9], t[3];
+  int has;
+};
+// computed once on the host (float64 -> float32 conversions are slow on the
+// device) and passed by value in the kernel arguments
+inline XfF32 xf32_host(const GdMesh& m) {
+  XfF32 x;
+  for (int i = 0; i < 9; ++i) x.r[i] = (float)m.rot[i];
+  for (int i = 0; i < 3; ++i) x.t[i] = (float)m.trans[i];
+  x.has = m.has_xf;
+  return x;
+}
 // Device-resident query state (lives at the start of the workspace).
 struct alignas(16) QState {
   Key128 best;                       // exact (distance, tri_a, tri_b) key
@@ -19,11 +36,13 @@ struct alignas(16) QState {
   int leaf_buf;                      // buffer holding the leaf-pair list
   unsigned long long n_in, n_out, n_leaf, n_band;
   unsigned long long n_cand;         // triangle-pair candidates (k_nfilter)
+  unsigned long long n_sel;          // band entries selected for the exact pass
   unsigned long long expanded, narrow, culled, band_eval;
   long long ov_cand, ov_in, ov_cap;
   float slack;
   int band_overflow;
   unsigned bar;                      // grid-barrier arrivals (k_traverse)
+  unsigned fbest;                    // best float32 narrow distance (ordered bits)
   unsigned long long cnt[kMaxIters + 1];       // survivors written by iteration i
   unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
   GdIterStat stats[kMaxIters];
@@ -33,6 +52,7 @@ struct alignas(16) QState {
 
 struct QArgs {
   GdMesh ma, mb;
+  XfF32 xa, xb;  // float32 transforms of ma, mb (xf32_host)
   GdBvh A, B;
   GdConfig cfg;
   QState* S;
@@ -91,23 +111,6 @@ __device__ __forceinline__ Box box_union(const Box& a, const Box& b) {
   return r;
 }
 
-// Rigid transform of a mesh in float32 (from GdMesh's float64 R, t).  Every
-// float32 vertex the traversal sees -- refit boxes, narrow filter --
-// goes through xf_apply on the staged float32 base vertex, so the boxes
-// contain exactly the vertices the narrow phase tests.
-struct XfF32 {
-  float r[9], t[3];
-  int has;
-};
-__device__ __forceinline__ XfF32 xf32_of(const GdMesh& m) {
-  XfF32 x;
-#pragma unroll
-  for (int i = 0; i < 9; ++i) x.r[i] = (float)m.rot[i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) x.t[i] = (float)m.trans[i];
-  x.has = m.has_xf;
-  return x;
-}
 __device__ __forceinline__ V3<float> xf_apply(const XfF32& x, const float4 v) {
   if (!x.has) return {v.x, v.y, v.z};
   return {fmaf(x.r[0], v.x, fmaf(x.r[1], v.y, fmaf(x.r[2], v.z, x.t[0]))),

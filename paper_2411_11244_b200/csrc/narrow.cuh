@@ -82,7 +82,7 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   const float* keys = q.key[buf];
   uint2* out = q.node[buf ^ 1];
   const bool culling = q.cfg.culling != 0;
-  const XfF32 xa = xf32_of(q.ma), xb = xf32_of(q.mb);
+  const XfF32 xa = q.xa, xb = q.xb;
   const int lane = threadIdx.x & 31;
   const float E = S->slack;
   float upd = 0.f;  // max query only
@@ -160,7 +160,10 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   }
   if (kMax && !kRescan) {
     upd = warp_max(upd);
-    if (lane == 0 && upd > 0.f) commit_bound<kMax>(S, upd);
+    if (lane == 0 && upd > 0.f) {
+      commit_bound<kMax>(S, upd);
+      atomicMax(&S->fbest, __float_as_uint(upd));
+    }
   }
   if (!kRescan) {
     tested = warp_sum_u64(tested);
@@ -178,7 +181,7 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   if (blockIdx.x * 256ull >= n) return;
   const uint2* cand = q.node[S->leaf_buf ^ 1];
   const float E = S->slack;
-  const XfF32 xa = xf32_of(q.ma), xb = xf32_of(q.mb);
+  const XfF32 xa = q.xa, xb = q.xb;
   __shared__ float warp_upd[8];
   float upd = kMax ? 0.f : INFINITY;
   unsigned long long tested = 0;
@@ -212,7 +215,13 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   if (threadIdx.x == 0) {
     float u = warp_upd[0];
     for (int w = 1; w < 8; ++w) u = kMax ? fmaxf(u, warp_upd[w]) : fminf(u, warp_upd[w]);
-    if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, u);
+    if (kMax ? u > 0.f : u < INFINITY) {
+      commit_bound<kMax>(S, u);
+      if (kMax)
+        atomicMax(&S->fbest, __float_as_uint(u));
+      else
+        atomicMin(&S->fbest, __float_as_uint(u));
+    }
   }
 }
 
@@ -223,47 +232,78 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
 template <bool kMax>
 __device__ void finalize(const QArgs& q);
 
+// Exact pass, step 1 (k_bandsel).  Band entries whose float32 distance f is
+// within E of the best float32 distance f_best (S->fbest, tracked where the
+// band is filled) can still attain the exact optimum: |f - exact| <= E/2 for
+// every pair, so an entry with f > f_best + E is exactly worse than the
+// f_best pair (min query; mirrored for max).  Survivors are compacted into
+// the (now idle) leaf-pair buffer so step 2 can spread them evenly.
 template <bool kMax>
-__global__ __launch_bounds__(256) void k_refine(QArgs q) {
+__global__ __launch_bounds__(256) void k_bandsel(QArgs q) {
   QState* S = q.S;
   const unsigned long long n = min(S->n_band, q.band_cap);
-  __shared__ Key128 wk[8];
-  __shared__ bool last;
-  if (blockIdx.x * 256ull < n) {
-    const float E = S->slack;
-    const float ub = load_bound(S);
-    Key128 best;
-    best.hi = ~0ull;
-    best.lo = ~0ull;
-    unsigned long long evals = 0;
-    for (unsigned long long i = blockIdx.x * 256ull + threadIdx.x; i < n; i += gridDim.x * 256ull) {
-      const float d = q.band_d[i];
-      if (kMax ? (d + E >= ub) : (d - E <= ub)) {
-        const uint2 ids = q.band_ids[i];
-        Key128 k = exact_key<kMax>(q, ids.x, ids.y);
-        if (key_less(k, best)) best = k;
-        ++evals;
-      }
+  const float E = S->slack;
+  const float fb = __uint_as_float(*reinterpret_cast<volatile unsigned*>(&S->fbest));
+  uint2* sel = q.node[S->leaf_buf];
+  const int lane = threadIdx.x & 31;
+  for (unsigned long long base = (unsigned long long)blockIdx.x * 256; base < n; base += gridDim.x * 256ull) {
+    const unsigned long long i = base + threadIdx.x;
+    bool cand = false;
+    if (i < n) {
+      const float f = q.band_d[i];
+      cand = kMax ? (f >= fb - E) : (f <= fb + E);  // +-inf (warm pair) always passes
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      Key128 other = shfl_key(best, o);
-      if (key_less(other, best)) best = other;
-    }
-    evals = warp_sum_u64(evals);
-    if ((threadIdx.x & 31) == 0) {
-      wk[threadIdx.x >> 5] = best;
-      if (evals) atomicAdd(&S->band_eval, evals);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < 8; ++w)
-        if (key_less(wk[w], best)) best = wk[w];
-      if (best.hi != ~0ull) atomic_min_key(&S->best, best);
+    const unsigned m = __ballot_sync(0xffffffffu, cand);
+    unsigned long long wbase = 0;
+    if (lane == 0 && m) wbase = atomicAdd(&S->n_sel, (unsigned long long)__popc(m));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (cand) {
+      const unsigned long long slot = wbase + __popc(m & ((1u << lane) - 1));
+      if (slot < q.cap) sel[slot] = q.band_ids[i];
     }
   }
-  // the last block to finish writes the witness and the result record
+}
+
+// Exact pass, step 2 (k_refine): one thread per selected pair (exact_key),
+// lexicographic 128-bit minimum; the last block to finish writes the witness
+// and the result record.  Small blocks: the selection is a few thousand to a
+// few ten thousand pairs, each a long float64 dependency chain.
+constexpr int kRefineThreads = 64;
+
+template <bool kMax>
+__global__ __launch_bounds__(kRefineThreads) void k_refine(QArgs q) {
+  QState* S = q.S;
+  const unsigned long long n = min(S->n_sel, q.cap);
+  const uint2* sel = q.node[S->leaf_buf];
+  __shared__ Key128 wk[kRefineThreads / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Key128 best;
+  best.hi = ~0ull;
+  best.lo = ~0ull;
+  unsigned long long evals = 0;
+  for (unsigned long long j = (unsigned long long)blockIdx.x * kRefineThreads + threadIdx.x; j < n;
+       j += (unsigned long long)gridDim.x * kRefineThreads) {
+    const uint2 ids = sel[j];
+    const Key128 k = exact_key<kMax>(q, ids.x, ids.y);
+    if (key_less(k, best)) best = k;
+    ++evals;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    Key128 other = shfl_key(best, o);
+    if (key_less(other, best)) best = other;
+  }
+  evals = warp_sum_u64(evals);
+  if (lane == 0) {
+    wk[wid] = best;
+    if (evals) atomicAdd(&S->band_eval, evals);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    for (int w = 1; w < kRefineThreads / 32; ++w)
+      if (key_less(wk[w], best)) best = wk[w];
+    if (best.hi != ~0ull) atomic_min_key(&S->best, best);
     __threadfence();
     last = atomicAdd(&S->done, 1u) == gridDim.x - 1;
   }

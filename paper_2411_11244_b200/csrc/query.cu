@@ -10,9 +10,10 @@
 //   k_ntest           float32 narrow phase on the candidates (min), fills the
 //                     exact-pass band
 //   k_nfilter<rescan> exits at once unless the band / candidate list overflowed
-//   k_refine          exact narrow phase (reference arithmetic, 64 or 32 bit)
-//                     over the band, lexicographic 128-bit key minimum; its
-//                     last block writes the witness points and the result
+//   k_bandsel         band entries within E of the best float32 distance
+//   k_refine          exact narrow phase (reference arithmetic, 64 or 32 bit),
+//                     one thread per selected pair, lexicographic 128-bit key
+//                     minimum; its last block writes the witness and result
 // The bound is a float32 cell carrying a slack E:
 // culling is conservative, so every pair that can attain the reference's
 // exact answer reaches the exact pass.
@@ -60,7 +61,7 @@ static void validate(const GdBvh& a, const GdBvh& b, const GdConfig& cfg) {
   GD_CHECK(cfg.front_hard_cap >= 4, GD_ERR_CONFIG, "front_hard_cap must be >= 4");
   GD_CHECK(a.depth >= 0 && a.depth <= 31 && b.depth >= 0 && b.depth <= 31, GD_ERR_INVALID,
            "tree depth out of range");
-  GD_CHECK(a.box && b.box && a.leaf_rec && b.leaf_rec && a.vtx32 && b.vtx32,
+  GD_CHECK(a.box && b.box && a.leaf_rec && b.leaf_rec && a.vtx32 && b.vtx32 && a.vmap && b.vmap,
            GD_ERR_INVALID, "BVH arrays must be allocated");
 }
 
@@ -131,11 +132,12 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
   if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
   mark(3);
   k_nfilter<kMax, true><<<sms * 8, 256, 0, s>>>(q);  // exits at once unless the band overflowed
-  k_refine<kMax><<<sms * 2, 256, 0, s>>>(q);          // + witness record in its last block
+  k_bandsel<kMax><<<sms, 256, 0, s>>>(q);
+  k_refine<kMax><<<sms * 4, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
   mark(4);
   mark(5);
   GD_CUDA(cudaGetLastError());
-  count_launches(kMax ? 4 : 5);
+  count_launches(kMax ? 5 : 6);
 }
 
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
@@ -148,6 +150,8 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   QArgs q;
   q.ma = ma;
   q.mb = mb;
+  q.xa = xf32_host(ma);
+  q.xb = xf32_host(mb);
   q.A = a;
   q.B = b;
   q.cfg = cfg;

@@ -1,14 +1,17 @@
 // refit.cu -- per-frame refit (bvh.py:242-306) fused with apply_transform
 // (mesh.py:102-105).
 //
-//   k_stage        float64 base vertex -> float32 float4 (once per base buffer)
-//   k_leaf_up      one thread per leaf: its 32-byte record, six staged vertex
-//                  gathers, float32 transform, leaf box = union of its 1..2
-//                  triangles; then the block folds its 256-leaf subtree 8
-//                  levels up in shared memory
-//   k_level_up     the same fold for the remaining top levels
-// Every node box is written exactly once; no level is re-read from HBM
-// except the <= 1/256 subtree roots handed from one fold to the next.
+//   k_stage        float64 base vertex -> float32 float4 at its staged slot
+//                  (first-use order, bvh_layout), once per base buffer
+//   k_leaf_vtx     per-leaf distinct vertex sets (also once per base buffer)
+//   k_refit        ONE launch per refit: one thread per leaf, its vertex set
+//                  streamed from three coalesced float4 planes, float32
+//                  transform, leaf box; each block folds its 256-leaf subtree
+//                  8 levels up (warp shuffles, staged coalesced stores); the
+//                  last-arriving block of every 256 sibling subtrees folds
+//                  their roots further (arrival counters), up to the root
+// Every node box is written exactly once; only the 1/256 subtree roots are
+// re-read (from L2) by the cascade.
 #include <algorithm>
 #include <vector>
 
@@ -18,56 +21,218 @@ namespace gd {
 
 constexpr int kFold = 256;  // nodes per block per fold (8 levels)
 
-__global__ __launch_bounds__(256) void k_stage(GdMesh m, float4* __restrict__ out) {
+__global__ __launch_bounds__(256) void k_stage(GdMesh m, const int32_t* __restrict__ vmap, float4* __restrict__ out) {
   const long long i = blockIdx.x * 256ll + threadIdx.x;
   if (i >= m.nv) return;
   const double* p = m.vtx + 3 * i;
-  out[i] = make_float4((float)p[0], (float)p[1], (float)p[2], 0.f);
+  out[vmap[i]] = make_float4((float)p[0], (float)p[1], (float)p[2], 0.f);
 }
 
-// fold `levels` levels inside the block; sb holds blockDim.x boxes of level
-// `lv`, the block covering nodes [first_rank, first_rank + blockDim.x)
-__device__ __forceinline__ void fold_up(float* box, Box* sb, Box mine, int lv, long long first_rank,
-                                        int levels) {
-  int width = blockDim.x;
-  sb[threadIdx.x] = mine;
-  for (int u = 0; u < levels; ++u) {
-    __syncthreads();
-    width >>= 1;
-    Box p;
-    const bool act = threadIdx.x < width;
-    if (act) p = box_union(sb[2 * threadIdx.x], sb[2 * threadIdx.x + 1]);
-    __syncthreads();
-    --lv;
-    first_rank >>= 1;
-    if (act) {
-      sb[threadIdx.x] = p;
-      store_box(box, ((1ull << lv) - 1) + first_rank + threadIdx.x, p);
+// union of this lane's box with the one `o` lanes up (mask: the block's lanes
+// when it is narrower than a warp; lanes whose source is outside never use it)
+__device__ __forceinline__ Box shfl_union(const Box& b, int o, unsigned mask) {
+  Box r;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    r.lo[k] = fminf(b.lo[k], __shfl_down_sync(mask, b.lo[k], o));
+    r.hi[k] = fmaxf(b.hi[k], __shfl_down_sync(mask, b.hi[k], o));
+  }
+  return r;
+}
+
+// The first nb (= 2^B <= blockDim.x) threads hold the boxes of nodes
+// [rank0, rank0 + nb) of level lv, one each.  Fold B levels up: warp
+// shuffles for the first five, the warp roots in warp 0 for the rest.  Level
+// u's nb >> u boxes are staged at sl[nb - (nb >> (u - 1)) ...]; one flat loop
+// then writes every staged box (three float2 each, consecutive threads ->
+// consecutive words of a level run).  All threads of the block must call it;
+// thread 0 returns the folded root.
+__device__ __forceinline__ Box fold_group(float* box, Box* sl, Box mine, int lv, unsigned rank0, int B) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nb = 1 << B;
+  if (threadIdx.x < nb) {
+    const unsigned mask = nb >= 32 ? 0xffffffffu : (1u << nb) - 1;
+    const int wl = min(B, 5);
+    for (int u = 1; u <= wl; ++u) {
+      mine = shfl_union(mine, 1 << (u - 1), mask);
+      if ((lane & ((1 << u) - 1)) == 0) sl[nb - (nb >> (u - 1)) + (threadIdx.x >> u)] = mine;
     }
+  }
+  if (B > 5) {
+    __syncthreads();
+    if (wid == 0) {
+      const int nw = nb >> 5;
+      mine = sl[nb - (nb >> 4) + (lane < nw ? lane : 0)];  // level-5 warp roots
+      for (int u = 6; u <= B; ++u) {
+        mine = shfl_union(mine, 1 << (u - 6), 0xffffffffu);
+        if (lane < nw && (lane & ((1 << (u - 5)) - 1)) == 0) sl[nb - (nb >> (u - 1)) + (lane >> (u - 5))] = mine;
+      }
+    }
+  }
+  __syncthreads();
+  const float2* s2 = reinterpret_cast<const float2*>(sl);
+  float2* d2 = reinterpret_cast<float2*>(box);
+  for (int j = threadIdx.x; j < 3 * (nb - 1); j += blockDim.x) {
+    const int t = j / 3, c = j - 3 * t;
+    const int u = B - (31 - __clz(nb - 1 - t));           // level of staged box t
+    const int i = t - (nb - (nb >> (u - 1)));              // index inside level u
+    const unsigned long long slot = (1ull << (lv - u)) + (rank0 >> u) + i;  // node (2^(lv-u) - 1) + r
+    d2[slot * 3 + c] = s2[j];
+  }
+  return mine;  // thread 0: the root of the folded subtree
+}
+
+// box written earlier in the same launch by another block: L2 load (.cg)
+__device__ __forceinline__ Box load_box_cg(const float* box, unsigned long long node) {
+  const float2* p = reinterpret_cast<const float2*>(box + (node + 1) * 6);
+  const float2 a = __ldcg(p), b = __ldcg(p + 1), c = __ldcg(p + 2);
+  Box r;
+  r.lo[0] = a.x; r.lo[1] = a.y; r.lo[2] = b.x;
+  r.hi[0] = b.y; r.hi[1] = c.x; r.hi[2] = c.y;
+  return r;
+}
+
+__device__ __forceinline__ void grow(Box& b, const V3<float>& p) {
+  b.lo[0] = fminf(b.lo[0], p.x);
+  b.lo[1] = fminf(b.lo[1], p.y);
+  b.lo[2] = fminf(b.lo[2], p.z);
+  b.hi[0] = fmaxf(b.hi[0], p.x);
+  b.hi[1] = fmaxf(b.hi[1], p.y);
+  b.hi[2] = fmaxf(b.hi[2], p.z);
+}
+
+// One launch refits the whole tree.  Each block: leaf boxes from the streamed
+// per-leaf vertex sets (three coalesced float4 planes; extras only for the
+// rare leaves with 5-6 distinct vertices), a coalesced leaf-box store, the
+// fold of its 256-leaf subtree.  Then a cascade: the last block of every
+// group of 256 (or fewer, at the top) sibling subtrees -- detected with a
+// per-group arrival counter -- folds their roots 8 levels further, until the
+// root.  The counters live at the end of leaf_x and are left zero.  The
+// vertices are the staged ones, so every box contains exactly the float32
+// vertices the narrow phase tests.
+__global__ __launch_bounds__(kFold) void k_refit(GdBvh T, XfF32 x) {
+  __shared__ __align__(16) Box sb[kFold], sl[kFold];
+  __shared__ bool last;
+  const unsigned L = (unsigned)T.leaf_count, W = (L + 31) >> 5;
+  const unsigned l = blockIdx.x * blockDim.x + threadIdx.x;  // leaf rank (< L exactly)
+  const float4* p = reinterpret_cast<const float4*>(T.leaf_vtx);
+  const float4 a = __ldg(p + l), b4 = __ldg(p + L + l), c = __ldg(p + 2 * L + l);
+  Box b;
+  const V3<float> v0 = xf_apply(x, make_float4(a.x, a.y, a.z, 0.f));
+  b.lo[0] = b.hi[0] = v0.x;
+  b.lo[1] = b.hi[1] = v0.y;
+  b.lo[2] = b.hi[2] = v0.z;
+  grow(b, xf_apply(x, make_float4(a.w, b4.x, b4.y, 0.f)));
+  grow(b, xf_apply(x, make_float4(b4.z, b4.w, c.x, 0.f)));
+  grow(b, xf_apply(x, make_float4(c.y, c.z, c.w, 0.f)));
+  const unsigned mask = __ldg(T.leaf_x + (l >> 5));
+  const int lane = threadIdx.x & 31;
+  if ((mask >> lane) & 1u) {
+    const unsigned rank = __ldg(T.leaf_x + W + (l >> 5)) + __popc(mask & ((1u << lane) - 1));
+    const float4* xv = reinterpret_cast<const float4*>(T.leaf_xvtx);
+    grow(b, xf_apply(x, __ldg(xv + 2 * rank)));
+    grow(b, xf_apply(x, __ldg(xv + 2 * rank + 1)));
+  }
+  // leaf boxes: coalesced float4 copy from shared memory (leaf slots L + l
+  // start 16-byte aligned for every block of >= 2 leaves)
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  const unsigned rank0 = blockIdx.x * blockDim.x;
+  {
+    const int nb = blockDim.x;
+    if (nb >= 2) {
+      const float4* s4 = reinterpret_cast<const float4*>(sb);
+      float4* d4 = reinterpret_cast<float4*>(T.box + ((unsigned long long)L + rank0) * 6);
+      for (int i = threadIdx.x; i < nb * 3 / 2; i += nb) d4[i] = s4[i];
+    } else {
+      store_box(T.box, (unsigned long long)(L - 1) + rank0, b);
+    }
+  }
+  int lv = T.depth;
+  const int B = 31 - __clz(blockDim.x);
+  if (B > 0) b = fold_group(T.box, sl, b, lv, rank0, B);
+  lv -= B;
+  unsigned rank = blockIdx.x;  // this block's subtree root: node rank at level lv
+  unsigned* cnt = T.leaf_x + 2 * W + 1;
+  while (lv > 0) {
+    // group of sibling subtree roots folded by its last-arriving block
+    const int g = min(lv, 8);
+    const unsigned gsize = 1u << g, group = rank >> g, ngroups = (1u << lv) >> g;
+    if (threadIdx.x == 0) {
+      // the only box another block reads: this subtree's root, published by
+      // thread 0 itself before its arrival
+      store_box(T.box, ((1ull << lv) - 1) + rank, b);
+      __threadfence();
+      last = atomicAdd(cnt + ngroups + group, 1u) == gsize - 1;
+      if (last) cnt[ngroups + group] = 0;  // ready for the next refit
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    Box mine = b;
+    if (threadIdx.x < gsize)
+      mine = load_box_cg(T.box, ((1ull << lv) - 1) + ((unsigned long long)group << g) + threadIdx.x);
+    b = fold_group(T.box, sl, mine, lv, group << g, g);  // the first gsize threads fold g levels
+    lv -= g;
+    rank = group;
   }
 }
 
-__global__ __launch_bounds__(kFold) void k_leaf_up(GdBvh T, GdMesh m, int levels) {
-  __shared__ Box sb[kFold];
-  const long long l = blockIdx.x * (long long)blockDim.x + threadIdx.x;  // leaf rank (< L exactly)
-  const XfF32 x = xf32_of(m);
-  const LeafRec r = load_leaf(T, l);
-  // both triangles unconditionally: a single-triangle leaf repeats triangle 0
-  const Box b = box_union(tri_box(leaf_tri32(T, x, r, 0)), tri_box(leaf_tri32(T, x, r, 1)));
-  store_box(T.box, (T.leaf_count - 1) + l, b);
-  fold_up(T.box, sb, b, T.depth, blockIdx.x * (long long)blockDim.x, levels);
-}
-
-__global__ __launch_bounds__(kFold) void k_level_up(float* box, int lv, int levels) {
-  __shared__ Box sb[kFold];
-  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  Box b = load_box(box, ((1ull << lv) - 1) + r);
-  fold_up(box, sb, b, lv, blockIdx.x * (long long)blockDim.x, levels);
+// per-leaf distinct vertex sets (gdist.h leaf_vtx / leaf_x / leaf_xvtx) from
+// the leaf records and the staged vertices
+__global__ __launch_bounds__(256) void k_leaf_vtx(GdBvh T) {
+  const long long l = blockIdx.x * 256ll + threadIdx.x;
+  const long long L = T.leaf_count, W = (L + 31) >> 5;
+  const int lane = threadIdx.x & 31;
+  int u[6];
+  int k = 0;
+  if (l < L) {
+    const LeafRec r = load_leaf(T, l);
+    const int s[6] = {r.r0.x, r.r0.y, r.r0.z, r.r0.w, r.r1.x, r.r1.y};
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      bool seen = false;
+#pragma unroll
+      for (int j = 0; j < i; ++j) seen = seen || (s[j] == s[i]);
+      if (!seen) u[k++] = s[i];
+    }
+    for (int i = k; i < 6; ++i) u[i] = u[0];
+    const float4* v = reinterpret_cast<const float4*>(T.vtx32);
+    const float4 a = v[u[0]], b = v[u[1]], c = v[u[2]], d = v[u[3]];
+    float4* p = reinterpret_cast<float4*>(T.leaf_vtx);
+    p[l] = make_float4(a.x, a.y, a.z, b.x);
+    p[L + l] = make_float4(b.y, b.z, c.x, c.y);
+    p[2 * L + l] = make_float4(c.z, d.x, d.y, d.z);
+  }
+  const bool extra = k > 4;
+  const unsigned mask = __ballot_sync(0xffffffffu, extra);
+  unsigned base = 0;
+  if (lane == 0) {
+    base = mask ? atomicAdd(&T.leaf_x[2 * W], (unsigned)__popc(mask)) : 0u;
+    if (l < L) {
+      T.leaf_x[l >> 5] = mask;
+      T.leaf_x[W + (l >> 5)] = base;
+    }
+  }
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (extra) {
+    const unsigned rank = base + __popc(mask & ((1u << lane) - 1));
+    const float4* v = reinterpret_cast<const float4*>(T.vtx32);
+    float4* x = reinterpret_cast<float4*>(T.leaf_xvtx);
+    x[2 * rank] = v[u[4]];
+    x[2 * rank + 1] = v[u[5]];
+  }
 }
 
 void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "mesh vertex count differs from the tree's");
-  if (m.nv > 0) k_stage<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, reinterpret_cast<float4*>(T.vtx32));
+  GD_CHECK(T.leaf_vtx && T.leaf_x && T.leaf_xvtx, GD_ERR_INVALID, "GdBvh leaf vertex sets must be allocated");
+  if (m.nv > 0)
+    k_stage<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, T.vmap, reinterpret_cast<float4*>(T.vtx32));
+  const long long W = (T.leaf_count + 31) / 32;
+  // extras counter + the refit's cascade counters (gdist.h leaf_x)
+  GD_CUDA(cudaMemsetAsync(T.leaf_x + 2 * W, 0, (1 + 2 * (T.leaf_count >> 16) + 4) * sizeof(uint32_t), s));
+  k_leaf_vtx<<<(unsigned)((T.leaf_count + 255) / 256), 256, 0, s>>>(T);
   GD_CUDA(cudaGetLastError());
 }
 
@@ -75,22 +240,11 @@ void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.m == T.n_tris, GD_ERR_TOPOLOGY,
            "refit mesh has " + std::to_string(m.m) + " triangles, tree was built over " + std::to_string(T.n_tris));
   GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "refit mesh vertex count differs from the build");
-  long long launches = 0;
   const long long L = T.leaf_count;
-  int lv = T.depth;
+  GD_CHECK(L < (1ll << 31), GD_ERR_INVALID, "tree too large for 32-bit leaf ranks");
   const int bs = (int)std::min<long long>(L, kFold);
-  const int lev = std::min(lv, __builtin_ctz((unsigned)bs));
-  k_leaf_up<<<(unsigned)(L / bs), bs, 0, s>>>(T, m, lev);
-  ++launches;
-  lv -= lev;
-  while (lv > 0) {
-    const long long cnt = 1ll << lv;
-    const int b2 = (int)std::min<long long>(cnt, kFold);
-    const int l2 = std::min(lv, __builtin_ctz((unsigned)b2));
-    k_level_up<<<(unsigned)(cnt / b2), b2, 0, s>>>(T.box, lv, l2);
-    ++launches;
-    lv -= l2;
-  }
+  k_refit<<<(unsigned)(L / bs), bs, 0, s>>>(T, xf32_host(m));
+  const long long launches = 1;
   GD_CUDA(cudaGetLastError());
   count_launches(launches);
 }
@@ -103,8 +257,10 @@ __global__ void k_export_leaf(GdMesh m, GdBvh B, T* nmin, T* nmax) {
   const long long l = blockIdx.x * 256ll + threadIdx.x;
   if (l >= B.leaf_count) return;
   const int4* rec = reinterpret_cast<const int4*>(B.leaf_rec) + 2 * l;
-  const int4 r0 = rec[0], r1 = rec[1];
-  const int v[6] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y};
+  const int4 r1 = rec[1];  // {b1, b2, tri0, tri1}: records hold staged slots, so use the triangle ids
+  const int32_t* i0 = m.tri + 3 * (long long)r1.z;
+  const int32_t* i1 = m.tri + 3 * (long long)(r1.w >= 0 ? r1.w : r1.z);
+  const int v[6] = {i0[0], i0[1], i0[2], i1[0], i1[1], i1[2]};
   const int nvert = r1.w >= 0 ? 6 : 3;
   T lo[3], hi[3];
   for (int c = 0; c < nvert; ++c) {

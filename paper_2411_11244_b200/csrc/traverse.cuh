@@ -124,6 +124,8 @@ __device__ void init_query(const QArgs& q) {
   S->n_leaf = 0;
   S->n_band = 0;
   S->n_cand = 0;
+  S->n_sel = 0;
+  S->fbest = kMax ? 0u : __float_as_uint(INFINITY);
   S->expanded = 0;
   S->narrow = 0;
   S->culled = 0;
@@ -159,8 +161,8 @@ __device__ void init_query(const QArgs& q) {
     const int32_t* ib = q.mb.tri + 3 * (long long)tb;
     // the pair always reaches the exact pass (band distance -inf / +inf);
     // its vertex-pair distance is an achieved distance, hence a valid bound
-    Tri<float> a = tri32(q.A, xf32_of(q.ma), ia[0], ia[1], ia[2]);
-    Tri<float> b = tri32(q.B, xf32_of(q.mb), ib[0], ib[1], ib[2]);
+    Tri<float> a = tri32(q.A, q.xa, q.A.vmap[ia[0]], q.A.vmap[ia[1]], q.A.vmap[ia[2]]);
+    Tri<float> b = tri32(q.B, q.xb, q.B.vmap[ib[0]], q.B.vmap[ib[1]], q.B.vmap[ib[2]]);
     commit_bound<kMax>(S, vertex_pair_bound<kMax>(a, b));
     q.band_ids[0] = make_uint2(ta, tb);
     q.band_d[0] = kMax ? INFINITY : -INFINITY;
