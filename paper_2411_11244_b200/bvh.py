@@ -162,6 +162,11 @@ class F12Bvh:
         self._leaf_xvtx = _lib.empty(2 * L * 4, torch.float32)
 
     def device_view(self) -> _lib.GdBvh:
+        """C view (include/gdist.h GdBvh), cached until a buffer changes."""
+        nv = self._vtx32.numel() // 4 if self._mesh is None else self._mesh.n_vertices
+        gv = getattr(self, "_gview", None)
+        if gv is not None and gv.vtx32 == self._vtx32.data_ptr() and gv.nv == nv:
+            return gv
         g = _lib.GdBvh()
         g.box = self._box.data_ptr()
         g.leaf_rec = self._leaf_rec.data_ptr()
@@ -172,8 +177,9 @@ class F12Bvh:
         g.leaf_xvtx = self._leaf_xvtx.data_ptr()
         g.leaf_count = self.leaf_count
         g.n_tris = len(self.prim_order)
-        g.nv = self._vtx32.numel() // 4 if self._mesh is None else self._mesh.n_vertices
+        g.nv = nv
         g.depth = self.depth
+        self._gview = g
         return g
 
     def _ensure_layout(self, mesh: TriangleMesh):
@@ -215,7 +221,7 @@ class F12Bvh:
         _lib.check(L.gd_bvh_sizes(len(self.prim_order), mesh.n_vertices, C.byref(sizes)), "bvh_sizes")
         ws = _lib.empty(max(int(sizes.build_workspace_bytes), 1), torch.uint8)
         g = mesh.device_view()
-        v = self.device_view()
+        v = _lib.GdBvh.from_buffer_copy(self.device_view())
         v.nv = mesh.n_vertices
         _lib.check(L.gd_bvh_layout(C.byref(g), C.byref(v), _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "bvh_layout")
         self._staged = mesh._root
@@ -229,7 +235,7 @@ class F12Bvh:
             self._write_records(mesh)
             return
         g = mesh.device_view()
-        v = self.device_view()
+        v = _lib.GdBvh.from_buffer_copy(self.device_view())
         v.nv = mesh.n_vertices
         _lib.check(_lib.lib().gd_stage_vertices(C.byref(g), C.byref(v), _lib.stream_ptr()), "stage_vertices")
         self._staged = mesh._root
@@ -311,7 +317,7 @@ def build_f12(mesh: TriangleMesh, dtype=np.float64) -> F12Bvh:
     torch = _lib.torch()
     ws = _lib.empty(max(int(sizes.build_workspace_bytes), 1), torch.uint8)
     g = src.device_view()
-    v = bvh.device_view()
+    v = _lib.GdBvh.from_buffer_copy(bvh.device_view())
     v.nv = src.n_vertices
     _lib.check(
         L.gd_bvh_build(C.byref(g), C.byref(v), _lib.ptr(ws), ws.numel(), bvh.prim_order.ctypes.data_as(C.c_void_p),

@@ -45,14 +45,17 @@ struct alignas(16) QState {
   unsigned fbest;                    // best float32 narrow distance (ordered bits)
   unsigned long long cnt[kMaxIters + 1];       // survivors written by iteration i
   unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
-  GdIterStat stats[kMaxIters];
+  GdResult res;                      // the result record, then the stats: one
+  GdIterStat stats[kMaxIters];       // contiguous device->host copy
   unsigned long long t_it[kMaxIters + 1];      // %globaltimer at iteration boundaries
+  unsigned long long t_sweep[kMaxIters];       // last block's sweep end (profiling)
 };
 
 
 struct QArgs {
   GdMesh ma, mb;
   XfF32 xa, xb;  // float32 transforms of ma, mb (xf32_host)
+  int profile;    // record per-iteration sweep times (gd_set_profiling)
   GdBvh A, B;
   GdConfig cfg;
   QState* S;

@@ -442,7 +442,8 @@ __device__ void finalize(const QArgs& q) {
       r.point_b[c] = pb[c];
     }
   }
-  *q.result = r;
+  S->res = r;
+  if (q.result) *q.result = r;
 }
 
 }  // namespace gd

@@ -18,6 +18,8 @@
 // culling is conservative, so every pair that can attain the reference's
 // exact answer reaches the exact pass.
 #include <algorithm>
+#include <cstddef>
+#include <cstring>
 
 #include "narrow.cuh"
 
@@ -90,11 +92,14 @@ int phase_ms(float* out, int n) {
   int k = 0;
   for (; k < 5 && k < n; ++k) GD_CUDA(cudaEventElapsedTime(out + k, g_ev[k], g_ev[k + 1]));
   if (g_last_state && n > 5) {
+    // per iteration: total, then (n > 5 + iterations) the sweep part
     int iters = 0;
-    unsigned long long t[kMaxIters + 1];
+    unsigned long long t[kMaxIters + 1], sw[kMaxIters];
     GD_CUDA(cudaMemcpy(&iters, &g_last_state->iter, sizeof(int), cudaMemcpyDeviceToHost));
     GD_CUDA(cudaMemcpy(t, g_last_state->t_it, sizeof(t), cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(sw, g_last_state->t_sweep, sizeof(sw), cudaMemcpyDeviceToHost));
     for (int i = 0; i < iters && k < n; ++i, ++k) out[k] = (float)((double)(t[i + 1] - t[i]) * 1e-6);
+    for (int i = 0; i < iters && k < n; ++i, ++k) out[k] = (float)((double)(sw[i] > t[i] ? sw[i] - t[i] : 0) * 1e-6);
   }
   return k;
 }
@@ -150,6 +155,7 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   QArgs q;
   q.ma = ma;
   q.mb = mb;
+  q.profile = g_profile ? 1 : 0;
   q.xa = xf32_host(ma);
   q.xb = xf32_host(mb);
   q.A = a;
@@ -164,7 +170,7 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   q.band_d = reinterpret_cast<float*>(base + L.band_d);
   q.cap = L.cap;
   q.band_cap = L.band_cap;
-  q.result = result_dev ? result_dev : reinterpret_cast<GdResult*>(base + L.result);
+  q.result = result_dev;  // nullptr: the record stays in the state block (QState::res)
   if (g_profile) g_last_state = q.S;
   if (cfg.kind == 1)
     launch_query<true>(q, s);
@@ -172,18 +178,25 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
     launch_query<false>(q, s);
 }
 
+static_assert(offsetof(QState, stats) == offsetof(QState, res) + sizeof(GdResult),
+              "result record and stats must be contiguous (one device->host copy)");
+
+// pinned staging for the single device->host copy of result + stats
+static thread_local char* g_pinned = nullptr;
+
 void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, GdResult* out, GdIterStat* stats,
                    int max_stats, cudaStream_t s) {
   WsLayout L = ws_layout(cfg);
   char* base = static_cast<char*>(ws);
-  const GdResult* src = result_dev ? result_dev : reinterpret_cast<const GdResult*>(base + L.result);
-  GD_CUDA(cudaMemcpyAsync(out, src, sizeof(GdResult), cudaMemcpyDeviceToHost, s));
-  if (stats && max_stats > 0) {
-    const QState* S = reinterpret_cast<const QState*>(base + L.state);
-    GD_CUDA(cudaMemcpyAsync(stats, S->stats, sizeof(GdIterStat) * std::min(max_stats, kMaxIters),
-                            cudaMemcpyDeviceToHost, s));
-  }
+  const QState* S = reinterpret_cast<const QState*>(base + L.state);
+  const size_t bytes = sizeof(GdResult) + sizeof(GdIterStat) * kMaxIters;
+  if (!g_pinned) GD_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&g_pinned), bytes, cudaHostAllocDefault));
+  const int ns = stats ? std::min(std::max(max_stats, 0), kMaxIters) : 0;
+  GD_CUDA(cudaMemcpyAsync(g_pinned, &S->res, sizeof(GdResult) + sizeof(GdIterStat) * ns, cudaMemcpyDeviceToHost, s));
+  if (result_dev) GD_CUDA(cudaMemcpyAsync(g_pinned, result_dev, sizeof(GdResult), cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaStreamSynchronize(s));
+  memcpy(out, g_pinned, sizeof(GdResult));
+  if (ns) memcpy(stats, g_pinned + sizeof(GdResult), sizeof(GdIterStat) * ns);
 }
 
 }  // namespace gd

@@ -125,6 +125,7 @@ __device__ void init_query(const QArgs& q) {
   S->n_band = 0;
   S->n_cand = 0;
   S->n_sel = 0;
+  for (int i = 0; i < kMaxIters; ++i) S->t_sweep[i] = 0;
   S->fbest = kMax ? 0u : __float_as_uint(INFINITY);
   S->expanded = 0;
   S->narrow = 0;
@@ -472,6 +473,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
       break;
     }
     expand_sweep<kMax>(q, sh, k1_stage, it, cur, n_in, k, ka, kb, to_leaves, ncand);
+    if (q.profile && threadIdx.x == 0) atomicMax(&S->t_sweep[it], globaltimer_ns());
     grid_barrier(&S->bar, ++phase);
     const unsigned long long n_out = V->cnt[it];
     if (n_out > (unsigned long long)q.cfg.front_hard_cap) {  // query.py:448-449

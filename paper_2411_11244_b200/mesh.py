@@ -49,7 +49,7 @@ class TriangleMesh:
 
     vertices: (n, 3) float64, triangles: (m, 3) int64, both read-only."""
 
-    __slots__ = ("_vertices", "_triangles", "_root", "_chain", "_rot", "_trans", "_dev", "__weakref__")
+    __slots__ = ("_vertices", "_triangles", "_root", "_chain", "_rot", "_trans", "_dev", "_gview", "__weakref__")
 
     def __init__(self, vertices, triangles):
         self._vertices, self._triangles = _validated(vertices, triangles)
@@ -58,6 +58,7 @@ class TriangleMesh:
         self._rot = None          # composed device transform (None = identity)
         self._trans = None
         self._dev = None
+        self._gview = None
 
     # -- lazily moved mesh (apply_transform) ------------------------------
     @classmethod
@@ -72,6 +73,7 @@ class TriangleMesh:
         out._rot = xf.rotation @ R0
         out._trans = xf.rotation @ t0 + xf.translation
         out._dev = None
+        out._gview = None
         return out
 
     @property
@@ -119,6 +121,9 @@ class TriangleMesh:
         return root._dev
 
     def device_view(self) -> _lib.GdMesh:
+        """C view (include/gdist.h GdMesh); cached -- the mesh is immutable."""
+        if self._gview is not None:
+            return self._gview
         vt, tr = self._upload()
         g = _lib.GdMesh()
         g.vtx = vt.data_ptr()
@@ -133,6 +138,7 @@ class TriangleMesh:
             g.rot[:] = [float(x) for x in self._rot.reshape(9)]
             g.trans[:] = [float(x) for x in self._trans.reshape(3)]
             g.has_xf = 1
+        self._gview = g
         return g
 
     def _geometry_key(self):

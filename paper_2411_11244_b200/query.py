@@ -281,25 +281,18 @@ def _check_build(cfg: EngineConfig, bvh_a: F12Bvh, bvh_b: F12Bvh) -> None:
 
 
 class PreparedQuery:
-    """A query bound to its meshes / trees / config: the device views and
-    workspace are resolved once, so repeated launches (frames, benches) cost
-    only the kernel sequence.  `launch()` is asynchronous; `collect()` does
-    the single device->host copy."""
+    """A query bound to its trees / config (and, per `bind`, meshes): the
+    device views and workspace are resolved once, so repeated launches
+    (frames, benches) cost only the kernel sequence.  `launch()` is
+    asynchronous; `collect()` does the single device->host copy."""
 
     def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, cfg: EngineConfig, kind: str, warm_pair=None):
         _check_build(cfg, bvh_a, bvh_b)
-        if warm_pair is not None:
-            ta, tb = int(warm_pair[0]), int(warm_pair[1])
-            if not (0 <= ta < mesh_a.n_triangles and 0 <= tb < mesh_b.n_triangles):
-                raise IndexError(f"warm_pair {warm_pair} out of range")
-        bvh_a.ensure_device(mesh_a)
-        bvh_b.ensure_device(mesh_b)
         self.kind = kind
-        self.meshes = (mesh_a, mesh_b)
+        self.warm_pair = warm_pair
         self.trees = (bvh_a, bvh_b)
-        self.g_ma, self.g_mb = mesh_a.device_view(), mesh_b.device_view()
-        self.g_a, self.g_b = bvh_a.device_view(), bvh_b.device_view()
         self.g_cfg = _gd_config(cfg, kind, warm_pair)
+        self.bind(mesh_a, mesh_b)
         nbytes = C.c_size_t(0)
         L = _lib.lib()
         _lib.check(L.gd_query_workspace_size(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg),
@@ -307,6 +300,20 @@ class PreparedQuery:
         self.ws = _Workspace.get(nbytes.value)
         self.res = _lib.GdResult()
         self.stats = (_lib.GdIterStat * _MAX_STATS)()
+
+    def bind(self, mesh_a, mesh_b):
+        """Point the query at (possibly moved) meshes of the same trees."""
+        bvh_a, bvh_b = self.trees
+        if self.warm_pair is not None:
+            ta, tb = int(self.warm_pair[0]), int(self.warm_pair[1])
+            if not (0 <= ta < mesh_a.n_triangles and 0 <= tb < mesh_b.n_triangles):
+                raise IndexError(f"warm_pair {self.warm_pair} out of range")
+        bvh_a.ensure_device(mesh_a)
+        bvh_b.ensure_device(mesh_b)
+        self.meshes = (mesh_a, mesh_b)
+        self.g_ma, self.g_mb = mesh_a.device_view(), mesh_b.device_view()
+        self.g_a, self.g_b = bvh_a.device_view(), bvh_b.device_view()
+        return self
 
     def launch(self, stream=None):
         _lib.check(_lib.lib().gd_query_async(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a),
@@ -322,6 +329,31 @@ class PreparedQuery:
     def run(self) -> QueryResult:
         self.launch()
         return self.collect()
+
+
+# recently used query plans, keyed by (trees, config, kind, warm pair, device);
+# the trees are held weakly
+_PLANS: "dict" = {}
+_PLANS_MAX = 16
+
+
+def _plan(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair) -> PreparedQuery:
+    import weakref
+
+    wp = None if warm_pair is None else (int(warm_pair[0]), int(warm_pair[1]))
+    key = (id(bvh_a), id(bvh_b), cfg, kind, wp, _lib.torch().cuda.current_device())
+    ent = _PLANS.get(key)
+    if ent is not None:
+        ra, rb, pq = ent
+        if ra() is bvh_a and rb() is bvh_b:
+            _check_build(cfg, bvh_a, bvh_b)
+            return pq.bind(mesh_a, mesh_b)
+    pq = PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, wp)
+    pq.trees = (weakref.proxy(bvh_a), weakref.proxy(bvh_b))
+    if len(_PLANS) >= _PLANS_MAX:
+        _PLANS.pop(next(iter(_PLANS)))
+    _PLANS[key] = (weakref.ref(bvh_a), weakref.ref(bvh_b), pq)
+    return pq
 
 
 def _result(kind: str, r: _lib.GdResult, stats) -> QueryResult:
@@ -342,7 +374,7 @@ def _result(kind: str, r: _lib.GdResult, stats) -> QueryResult:
 
 
 def _run_query(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair=None) -> QueryResult:
-    return PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair).run()
+    return _plan(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair).run()
 
 
 def run_min_query(mesh_a: TriangleMesh, mesh_b: TriangleMesh, bvh_a: F12Bvh, bvh_b: F12Bvh,

@@ -53,8 +53,10 @@ for warm in (None, "self"):
            "phases_ms": dict(zip(["init", "expand", "narrow", "exact", "final"], [round(x, 4) for x in ph[:5]])),
            "expanded": r.expanded_pairs, "narrow_pairs": r.narrow_pairs, "band": r.band_pairs,
            "iters": [{"k": s.k, "in": s.front_in, "out": s.front_out, "culled": s.culled,
-                      "bound": round(s.bound_after, 6), "ms": round(ph[5 + i], 4) if 5 + i < len(ph) else None}
+                      "bound": round(s.bound_after, 6), "ms": round(ph[5 + i], 4) if 5 + i < len(ph) else None,
+                      "sweep_ms": round(ph[5 + len(r.iterations) + i], 4)
+                      if 5 + len(r.iterations) + i < len(ph) else None}
                      for i, s in enumerate(r.iterations)],
-           "tail_ms": [round(x, 4) for x in ph[5 + len(r.iterations):]]}
+           }
     print(json.dumps(out))
 torch.cuda.synchronize()

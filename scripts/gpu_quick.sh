@@ -15,5 +15,5 @@ for f in ['gpurun_out/exp_min.log', 'gpurun_out/exp_max.log']:
         d = json.loads(line)
         if d['warm']: continue
         print(d['distance'], d['witness'], d['phases_ms'], 'narrow_pairs', d['narrow_pairs'])
-        print('   ', [(i['in'], i['ms']) for i in d['iters']])
+        print('   ', [(i['in'], i['ms'], i['sweep_ms']) for i in d['iters']])
 PY
