@@ -50,18 +50,22 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False) -> Path:
-    """Compile every source to an object (in parallel) and link libgdist.so."""
+def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = False, defines=(), out: Path | None = None
+          ) -> Path:
+    """Compile every source to an object (in parallel) and link libgdist.so
+    (`defines` / `out`: an experiment variant, objects kept apart)."""
     nvcc = _nvcc()
-    BUILD.mkdir(exist_ok=True)
+    objdir = BUILD if not defines else BUILD / ("v_" + "_".join(d.replace("=", "-") for d in defines))
+    lib_out = out or LIB
+    objdir.mkdir(parents=True, exist_ok=True)
     headers = _headers()
     jobs = []
     objs = []
     for src in _sources():
-        obj = BUILD / (src.name + ".o")
+        obj = objdir / (src.name + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *headers, Path(__file__)]):
-            flags = list(NVCC_FLAGS)
+            flags = list(NVCC_FLAGS) + [f"-D{d}" for d in defines]
             if ptxas_verbose and src.suffix == ".cu":
                 flags += ["-Xptxas", "-v"]
             jobs.append([nvcc, *flags, "-c", str(src), "-o", str(obj)])
@@ -76,11 +80,11 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as pool:
         list(pool.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or jobs or _stale(lib_out, objs):
+        tmp = lib_out.with_suffix(".so.tmp")
         run([nvcc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcudart"])
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":

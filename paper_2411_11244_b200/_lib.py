@@ -16,7 +16,7 @@ from pathlib import Path
 
 from .errors import ConfigError, FrontOverflowError, MeshDistError, TopologyMismatchError
 
-_LIB_PATH = Path(__file__).resolve().parent / "libgdist.so"
+_LIB_PATH = Path(__file__).resolve().parent / os.environ.get("GDIST_LIB_VARIANT", "libgdist.so")
 
 GD_OK = 0
 GD_ERR_INVALID = 1

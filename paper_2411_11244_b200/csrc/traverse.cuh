@@ -5,7 +5,7 @@
 
 namespace gd {
 
-constexpr int kExpandThreads = 256;
+constexpr int kExpandThreads = 256;  // 4 blocks / SM: one block's tile flush overlaps the others' sweep
 constexpr int kGenericItems = 1;                                   // candidates / thread / tile (k >= 2)
 constexpr int kGenericTile = kExpandThreads * kGenericItems;
 constexpr int kK1Rounds = 4;                                       // entries / thread / tile (k == 1)
@@ -191,21 +191,21 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-// fence / arrive / spin (relaxed) / fence: the pattern of a cooperative-groups
-// grid sync.  Data written in the same launch (fronts, counters) is read with
-// plain coherent loads after it, never through the non-coherent __ldg path.
+// release-arrive / acquire-spin: every block's writes before the barrier are
+// visible to every block after it.  Data written in the same launch (fronts,
+// counters) is read with plain coherent loads, never through __ldg.
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned target = phase * gridDim.x;
-    __threadfence();
-    atomicAdd(bar, 1u);
-    while (*reinterpret_cast<volatile unsigned*>(bar) < target) __nanosleep(32);
-    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }
-
 
 // One expansion sweep (query.py:349-451, Alg. 2) over front `cur`.  Two
 // mappings, chosen uniformly per iteration from the adaptive depth k:
@@ -221,7 +221,11 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
                                              bool to_leaves, unsigned long long ncand) {
   QState* S = q.S;
   const int shift = ka + kb;
+#ifdef GD_K1_GENERIC
+  const bool k1 = false;
+#else
   const bool k1 = (k == 1);
+#endif
   const unsigned long long tiles = k1 ? (n_in + kK1Tile - 1) / kK1Tile : (ncand + kGenericTile - 1) / kGenericTile;
   const uint2* __restrict__ in_node = q.node[cur];
   const float* __restrict__ in_key = q.key[cur];
