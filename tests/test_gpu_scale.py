@@ -1,0 +1,162 @@
+"""Parity beyond desk size (GPU).
+
+* Mid-size rings (50K triangles per mesh, rotation-sequence frames) against the
+  CPU oracle on the SAME tree topology: bitwise distances and witnesses when
+  both sides see the same float64 vertices, 1e-12 through the lazy device
+  transform; float32 engine precision bitwise against the oracle's float32 run.
+* Full-size rings (config 2, 2 x 7.5M triangles): size-independent properties
+  -- determinism, A/B swap symmetry, the witness pair's exact distance, a
+  million sampled pairs never closer (farther) than the answer, and a local
+  brute force around the witness.
+* The band-overflow rescan path and far-from-origin coordinates.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_trees(oracle, bvh_a, bvh_b, va, ta, vb, tb, dtype=np.float64):
+    trees = []
+    for bvh, v, t in ((bvh_a, va, ta), (bvh_b, vb, tb)):
+        tr = oracle.Tree(np.empty((bvh.n_nodes, 3), dtype=dtype), np.empty((bvh.n_nodes, 3), dtype=dtype),
+                         np.asarray(bvh.leaf_tris), np.asarray(bvh.prim_order), bvh.depth)
+        trees.append(oracle.fill_boxes(tr, v, t))
+    return trees
+
+
+def _tie_ok(oracle, got, want, pa, pb, kind):
+    """identical witness, or a documented tie: our (lexicographically first
+    brute-force) pair attains the reference distance exactly"""
+    if (got.witness.tri_a, got.witness.tri_b) == (want.tri_a, want.tri_b):
+        return True
+    fn = oracle.tri_tri_min if kind == "min" else oracle.tri_tri_max
+    d = fn(pa[[got.witness.tri_a]], pb[[got.witness.tri_b]])[0][0]
+    return d == want.distance and (got.witness.tri_a, got.witness.tri_b) < (want.tri_a, want.tri_b)
+
+
+@pytest.mark.parametrize("frame", [0, 333])
+def test_rings_50k_vs_oracle(md, gpu, oracle, frame):
+    tz, tbase = md.ring_pair_base(250, 100)
+    xa, xb = md.ring_frame_transforms(frame)
+    lazy_a, lazy_b = md.apply_transform(tz, xa), md.apply_transform(tbase, xb)
+    # materialised meshes: both sides see numpy's float64 vertices
+    a, b = md.TriangleMesh(lazy_a.vertices, lazy_a.triangles), md.TriangleMesh(lazy_b.vertices, lazy_b.triangles)
+    ta, tb = md.build_f12(tz), md.build_f12(tbase)
+    oa, ob = _oracle_trees(oracle, ta, tb, a.vertices, a.triangles, b.vertices, b.triangles)
+    pa, pb = a.triangle_points(), b.triangle_points()
+    cfg = oracle.Config(workers=os.cpu_count() or 1)
+    for kind in ("min", "max"):
+        run = md.run_min_query if kind == "min" else md.run_max_query
+        want = oracle.run_query(oa, ob, pa, pb, kind, cfg)
+        md.refit(ta, a)
+        md.refit(tb, b)
+        got = run(a, b, ta, tb)
+        assert got.distance == want.distance, (kind, got.distance, want.distance)
+        assert _tie_ok(oracle, got, want, pa, pb, kind)
+        # the lazy device transform: within 1e-12 of the reference's dgemm vertices
+        md.refit(ta, lazy_a)
+        md.refit(tb, lazy_b)
+        lazy = run(lazy_a, lazy_b, ta, tb)
+        assert abs(lazy.distance - want.distance) <= 1e-12 * want.distance
+        assert (lazy.witness.tri_a, lazy.witness.tri_b) == (got.witness.tri_a, got.witness.tri_b)
+
+
+def test_rings_50k_precision32(md, gpu, oracle):
+    tz, tbase = md.ring_pair_base(250, 100)
+    xa, xb = md.ring_frame_transforms(71)
+    a = md.TriangleMesh(md.apply_transform(tz, xa).vertices, tz.triangles)
+    b = md.TriangleMesh(md.apply_transform(tbase, xb).vertices, tbase.triangles)
+    ta, tb = md.build_f12(a, dtype=np.float32), md.build_f12(b, dtype=np.float32)
+    oa, ob = _oracle_trees(oracle, ta, tb, a.vertices, a.triangles, b.vertices, b.triangles, np.float32)
+    pa, pb = a.triangle_points(np.float32), b.triangle_points(np.float32)
+    cfg32 = md.EngineConfig(precision=32)
+    ocfg = oracle.Config(precision=32, workers=os.cpu_count() or 1)
+    for kind in ("min", "max"):
+        want = oracle.run_query(oa, ob, pa, pb, kind, ocfg)
+        got = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb, cfg32)
+        assert got.distance == want.distance, kind
+        assert _tie_ok(oracle, got, want, pa, pb, kind)
+
+
+def test_far_from_origin(md, gpu, oracle):
+    """The slack scales with the coordinates: a scene 1e3 away from the
+    origin still returns the reference's exact answer."""
+    a0, b0 = md.gen_scene("interlocked-rings", {"nu": 40, "nv": 20})
+    off = md.RigidTransform(np.eye(3), (1000.0, -2000.0, 500.0))
+    a = md.TriangleMesh(md.apply_transform(a0, off).vertices, a0.triangles)
+    b = md.TriangleMesh(md.apply_transform(b0, off).vertices, b0.triangles)
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    pa, pb = a.triangle_points(), b.triangle_points()
+    for kind in ("min", "max"):
+        d, ia, ib, _, _ = oracle.brute_force(pa, pb, kind, force=True)
+        got = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb)
+        assert got.distance == d and (got.witness.tri_a, got.witness.tri_b) == (ia, ib), kind
+
+
+def test_band_overflow_rescan(md, gpu):
+    """A 2-entry exact-pass band overflows; the rescan pass re-filters every
+    leaf pair with the final bound and still returns the exact answer."""
+    from paper_2411_11244_b200 import query as Q
+
+    a, b = md.gen_scene("interlocked-rings", {"nu": 100, "nv": 50})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    for kind in ("min", "max"):
+        base = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb)
+        pq = Q.PreparedQuery(a, b, ta, tb, md.EngineConfig(), kind)
+        pq.g_cfg.band_cap = 2
+        r = pq.run()
+        assert r.distance == base.distance
+        assert (r.witness.tri_a, r.witness.tri_b) == (base.witness.tri_a, base.witness.tri_b)
+        assert r.witness.point_a.tolist() == base.witness.point_a.tolist()
+
+
+@pytest.fixture(scope="module")
+def rings_full(md):
+    tz, tbase = md.ring_pair_base(2500, 1500)
+    ta, tb = md.build_f12(tz), md.build_f12(tbase)
+    xa, xb = md.ring_frame_transforms(7)
+    # materialised (numpy float64) vertices: every check below sees exactly
+    # the vertices the device query sees
+    a = md.TriangleMesh(md.apply_transform(tz, xa).vertices, tz.triangles)
+    b = md.TriangleMesh(md.apply_transform(tbase, xb).vertices, tbase.triangles)
+    return a, b, ta, tb, a.triangle_points(), b.triangle_points()
+
+
+@pytest.mark.parametrize("kind", ["min", "max"])
+def test_rings_full_size_properties(md, gpu, rings_full, kind):
+    a, b, ta, tb, pa, pb = rings_full
+    cfg = md.EngineConfig(front_hard_cap=1 << 27)
+    run = md.run_min_query if kind == "min" else md.run_max_query
+    md.refit(ta, a)
+    md.refit(tb, b)
+    r1, r2 = run(a, b, ta, tb, cfg), run(a, b, ta, tb, cfg)
+    # determinism
+    assert r1.distance == r2.distance and (r1.witness.tri_a, r1.witness.tri_b) == (r2.witness.tri_a, r2.witness.tri_b)
+    # A/B swap symmetry (the witness rule is lexicographic in (tri_a, tri_b),
+    # so only the distance is compared)
+    rs = run(b, a, tb, ta, cfg)
+    assert rs.distance == r1.distance
+    # the witness pair attains the distance (reference arithmetic, float64)
+    fn = md.tri_tri_min if kind == "min" else md.tri_tri_max
+    assert fn(pa[r1.witness.tri_a], pb[r1.witness.tri_b])[0] == r1.distance
+    # a million random pairs are never closer (min) / farther (max)
+    rng = np.random.default_rng(11)
+    ia = rng.integers(0, a.n_triangles, 1_000_000)
+    ib = rng.integers(0, b.n_triangles, 1_000_000)
+    batch = md.batch_tri_tri_min if kind == "min" else md.batch_tri_tri_max
+    d = batch(pa[ia], pb[ib])[0]
+    assert (d >= r1.distance).all() if kind == "min" else (d <= r1.distance).all()
+    if kind == "min":
+        # local brute force around the witness: every pair of triangles whose
+        # centroids lie within 0.03 of the witness points
+        sa = np.flatnonzero(np.linalg.norm(pa.mean(axis=1) - r1.witness.point_a, axis=1) < 0.03)
+        sb = np.flatnonzero(np.linalg.norm(pb.mean(axis=1) - r1.witness.point_b, axis=1) < 0.03)
+        assert r1.witness.tri_a in sa and r1.witness.tri_b in sb
+        dl, wl = md.brute_force_min(md.TriangleMesh(a.vertices, a.triangles[sa]),
+                                    md.TriangleMesh(b.vertices, b.triangles[sb]), force=True)
+        assert dl == r1.distance
+        assert (sa[wl.tri_a], sb[wl.tri_b]) == (r1.witness.tri_a, r1.witness.tri_b)
