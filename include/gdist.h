@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 4
+#define GDIST_ABI_VERSION 5
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -119,6 +119,14 @@ typedef struct GdConfig {
   int64_t warm_a;            /* warm_pair triangle ids, -1 = none          */
   int64_t warm_b;
   int64_t band_cap;          /* exact-pass candidate buffer entries, 0 = default */
+  /* split query (multi-GPU): with split_world > 1 this call
+   * expands only the node pairs whose ancestor pair at tree level
+   * split_level (clamped to each tree's depth) hashes to split_rank; the
+   * exact answers of the split_world calls combine lexicographically. */
+  int32_t split_rank;
+  int32_t split_world;       /* 0 or 1 = no split                            */
+  int32_t split_level;
+  int32_t _pad;
 } GdConfig;
 
 /* QueryResult (query.py:230-263) + Witness (query.py:136-144). */

@@ -57,6 +57,7 @@ from .query import (
     run_max_query,
     run_min_query,
 )
+from .parallel import run_sequence, run_split_query
 from .scenes import gen_scene, ring_frame_transforms, ring_pair_base, scene_kinds, torus_mesh
 
 __version__ = "0.1.0"
@@ -156,6 +157,8 @@ __all__ = [
     "run_dfs_baseline",
     "run_max_query",
     "run_min_query",
+    "run_sequence",
+    "run_split_query",
     "scene_kinds",
     "torus_mesh",
     "tri_tri_max",

@@ -81,6 +81,10 @@ class GdConfig(C.Structure):
         ("warm_a", C.c_int64),
         ("warm_b", C.c_int64),
         ("band_cap", C.c_int64),
+        ("split_rank", C.c_int32),
+        ("split_world", C.c_int32),
+        ("split_level", C.c_int32),
+        ("_pad", C.c_int32),
     ]
 
 

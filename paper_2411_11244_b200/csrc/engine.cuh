@@ -45,6 +45,7 @@ struct alignas(16) QState {
   unsigned fbest;                    // best float32 narrow distance (ordered bits)
   unsigned long long cnt[kMaxIters + 1];       // survivors written by iteration i
   unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
+  unsigned long long skip_it[kMaxIters];       // candidates of pairs another split rank owns
   GdResult res;                      // the result record, then the stats: one
   GdIterStat stats[kMaxIters];       // contiguous device->host copy
   unsigned long long t_it[kMaxIters + 1];      // %globaltimer at iteration boundaries

@@ -95,6 +95,19 @@ __device__ __forceinline__ float vertex_pair_bound(const Tri<float>& a, const Tr
 }
 
 // ---------------------------------------------------------------------------
+// split query: owner rank of a node pair at depths (da, db) -- the hash of
+// its ancestor pair at (la, lb) (gdist.h GdConfig.split_*); every descendant
+// of an owned pair is owned, so the test is idempotent once da >= la, db >= lb
+__device__ __forceinline__ bool owned(const GdConfig& c, unsigned na, unsigned nb, int da, int db, int la, int lb) {
+  if (c.split_world <= 1 || da < la || db < lb) return true;
+  const unsigned aa = ((na + 1) >> (da - la)) - 1, ab = ((nb + 1) >> (db - lb)) - 1;
+  unsigned h = aa * 0x9E3779B1u ^ (ab + 0x7F4A7C15u) * 0x85EBCA77u;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 13;
+  return (int)(h % (unsigned)c.split_world) == c.split_rank;
+}
+
 // query prologue (one thread; k_traverse block 0 before its first barrier):
 // root key and bound, slack, root front, counters, warm_pair
 template <bool kMax>
@@ -134,7 +147,7 @@ __device__ void init_query(const QArgs& q) {
   S->band_overflow = 0;
   S->ov_cand = S->ov_in = S->ov_cap = 0;
   for (int i = 0; i <= kMaxIters; ++i) S->cnt[i] = 0;
-  for (int i = 0; i < kMaxIters; ++i) S->culled_it[i] = 0;
+  for (int i = 0; i < kMaxIters; ++i) S->culled_it[i] = S->skip_it[i] = 0;
   q.node[0][0] = make_uint2(0, 0);
   q.key[0][0] = key0;
   if (q.A.depth == 0 && q.B.depth == 0) {
@@ -218,7 +231,8 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned phase) {
 template <bool kMax>
 __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, unsigned char* k1_stage, int it,
                                              int cur, unsigned long long n_in, int k, int ka, int kb,
-                                             bool to_leaves, unsigned long long ncand) {
+                                             bool to_leaves, unsigned long long ncand, int da, int db, int la,
+                                             int lb) {
   QState* S = q.S;
   const int shift = ka + kb;
 #ifdef GD_K1_GENERIC
@@ -235,7 +249,7 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
   const unsigned leaf_a0 = (unsigned)((1ull << q.A.depth) - 1), leaf_b0 = (unsigned)((1ull << q.B.depth) - 1);
   const unsigned ra0 = to_leaves ? leaf_a0 : 0u, rb0 = to_leaves ? leaf_b0 : 0u;  // output index base
   const bool culling = q.cfg.culling != 0, enh = q.cfg.enhanced_bounds != 0;
-  unsigned long long my_culled = 0;
+  unsigned long long my_culled = 0, my_skipped = 0;  // skipped: not owned (split query)
 
   if (k1) {
     // survivors are staged in shared memory (warp-aggregated appends), then
@@ -275,7 +289,9 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
         }
         unsigned keep = 0;
         float keys[4];
-        if (e < t1) {
+        const bool mine = e < t1 && owned(q.cfg, nd.x, nd.y, da, db, la, lb);
+        if (e < t1 && !mine) my_skipped += (unsigned)(ca * cb);
+        if (mine) {
           // stale-entry re-cull: descendants' keys are monotone in the parent's
           if (culling && !survives<kMax>(pk, ub)) {
             my_culled += (unsigned)(ca * cb);
@@ -382,6 +398,10 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
         const unsigned long long e = t >> shift, off = t & off_mask;
         const float pk = in_key[e];
         const uint2 nd = in_node[e];
+        if (!owned(q.cfg, nd.x, nd.y, da, db, la, lb)) {
+          ++my_skipped;
+          continue;
+        }
         if (culling && !survives<kMax>(pk, ub)) {
           ++my_culled;
           continue;
@@ -432,7 +452,11 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
 
   // --- per-block counters -----------------------------------------------------
   unsigned long long c = warp_sum_u64(my_culled);
-  if ((threadIdx.x & 31) == 0) sh.red_culled[threadIdx.x >> 5] = c;
+  const unsigned long long sk = q.cfg.split_world > 1 ? warp_sum_u64(my_skipped) : 0ull;
+  if ((threadIdx.x & 31) == 0) {
+    sh.red_culled[threadIdx.x >> 5] = c;
+    if (sk) atomicAdd(&S->skip_it[it], sk);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     unsigned long long bc = 0;
@@ -458,6 +482,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
   unsigned long long n_in = V->n_in;
   int it = V->iter, cur = 0, da = 0, db = 0;
   unsigned long long expanded = 0;
+  const int la = min(q.cfg.split_level, q.A.depth), lb = min(q.cfg.split_level, q.B.depth);
   if (rec) S->t_it[it] = globaltimer_ns();
   while (n_in > 0 && it < kMaxIters) {
     const int ra = q.A.depth - da, rb = q.B.depth - db;
@@ -476,7 +501,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
       n_in = 0;
       break;
     }
-    expand_sweep<kMax>(q, sh, k1_stage, it, cur, n_in, k, ka, kb, to_leaves, ncand);
+    expand_sweep<kMax>(q, sh, k1_stage, it, cur, n_in, k, ka, kb, to_leaves, ncand, da, db, la, lb);
     if (q.profile && threadIdx.x == 0) atomicMax(&S->t_sweep[it], globaltimer_ns());
     grid_barrier(&S->bar, ++phase);
     const unsigned long long n_out = V->cnt[it];
@@ -490,7 +515,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
       n_in = 0;
       break;
     }
-    expanded += ncand;
+    expanded += ncand - V->skip_it[it];  // candidates of the pairs this call owns
     if (rec) {
       S->t_it[it + 1] = globaltimer_ns();
       GdIterStat st;

@@ -1,0 +1,166 @@
+"""Multi-GPU drivers (the reference is single-process,
+query.py:426-433 parallelises only over CPU threads).
+
+* Frames of a rotation / trajectory sequence are independent: each rank (one
+  process per GPU, torch.distributed) holds full replicas of both meshes and
+  trees and evaluates frames f = rank, rank + world, ...; one all-gather at the
+  end assembles every frame's (distance, tri_a, tri_b) on every rank.  No
+  collective inside the frame loop ("scaling": "weak").
+* A single large query is split by dealing the BVTT node pairs to the ranks
+  by a hash of their ancestor pair at a fixed tree level (`split_level`,
+  independent of each rank's adaptive-depth schedule); every rank expands its
+  part independently -- its own bound is a valid global bound, so every pair
+  that can attain the optimum survives on its owner -- and the exact answers
+  are combined with the reference's lexicographic witness rule
+  (query.py:205-220) in one all-gather.
+
+The collective plumbing is torch.distributed (NCCL on GPUs, gloo in the CPU
+tests); the per-frame / per-part compute is libgdist's.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+def world_info(group=None) -> tuple[int, int]:
+    """(rank, world size) of `group`, (0, 1) without torch.distributed."""
+    dist = _dist()
+    if not (dist.is_available() and dist.is_initialized()):
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def frames_of_rank(n_frames: int, rank: int, world: int) -> range:
+    """Frames owned by `rank`: f = rank (mod world)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    return range(rank, n_frames, world)
+
+
+def gather_frames(n_frames: int, local: dict, group=None, device=None) -> np.ndarray:
+    """Assemble per-frame results (f -> (distance, tri_a, tri_b)) computed on
+    the ranks into one (n_frames, 3) float64 array on every rank (one
+    all-gather of a fixed-size padded tensor)."""
+    import torch
+
+    rank, world = world_info(group)
+    per = math.ceil(n_frames / world) if n_frames else 0
+    buf = torch.full((per, 4), -1.0, dtype=torch.float64)
+    for i, f in enumerate(frames_of_rank(n_frames, rank, world)):
+        d, ta, tb = local[f]
+        buf[i] = torch.tensor([float(f), float(d), float(ta), float(tb)], dtype=torch.float64)
+    if world == 1:
+        rows = buf
+    else:
+        dist = _dist()
+        dev = device if device is not None else (torch.device("cuda", torch.cuda.current_device())
+                                                  if dist.get_backend(group) == "nccl" else torch.device("cpu"))
+        buf = buf.to(dev)
+        out = torch.empty((world * per, 4), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(out, buf, group=group)
+        rows = out.cpu()
+    res = np.full((n_frames, 3), np.nan)
+    for f, d, ta, tb in rows.numpy():
+        if f >= 0:
+            res[int(f)] = (d, ta, tb)
+    return res
+
+
+def run_frames(n_frames: int, frame_fn, group=None, device=None) -> np.ndarray:
+    """Evaluate frame_fn(f) -> (distance, tri_a, tri_b) for this rank's frames
+    and gather all frames on every rank."""
+    rank, world = world_info(group)
+    local = {f: frame_fn(f) for f in frames_of_rank(n_frames, rank, world)}
+    return gather_frames(n_frames, local, group, device)
+
+
+def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cfg=None, group=None) -> np.ndarray:
+    """Distance over a rigid-motion sequence, frames sharded over the ranks.
+
+    transforms: list of (xf_a, xf_b) RigidTransform pairs (either may be
+    None = identity).  Every rank holds both meshes and trees; returns the
+    (n_frames, 3) array of (distance, tri_a, tri_b) on every rank."""
+    from .bvh import refit
+    from .mesh import apply_transform
+    from .query import run_max_query, run_min_query
+
+    run = run_min_query if kind == "min" else run_max_query
+
+    def frame(f):
+        xa, xb = transforms[f]
+        a = mesh_a if xa is None else apply_transform(mesh_a, xa)
+        b = mesh_b if xb is None else apply_transform(mesh_b, xb)
+        refit(bvh_a, a)
+        refit(bvh_b, b)
+        r = run(a, b, bvh_a, bvh_b, cfg)
+        w = r.witness
+        return r.distance, (-1 if w is None else w.tri_a), (-1 if w is None else w.tri_b)
+
+    return run_frames(len(transforms), frame, group)
+
+
+def combine_parts(kind: str, parts: list) -> tuple:
+    """Combine per-rank exact answers (distance, tri_a, tri_b) of a split
+    query with the reference's rule: best distance, then the
+    lexicographically smallest (tri_a, tri_b) (query.py:205-220)."""
+    found = [p for p in parts if p[1] >= 0]
+    if not found:
+        return parts[0]
+    if kind == "min":
+        return min(found, key=lambda p: (p[0], p[1], p[2]))
+    return min(found, key=lambda p: (-p[0], p[1], p[2]))
+
+
+def run_split_query(mesh_a, mesh_b, bvh_a, bvh_b, kind: str = "min", cfg=None, group=None, split_level: int = 5,
+                    rank: int | None = None, world: int | None = None):
+    """One query split over the ranks of `group` (or, with explicit
+    rank / world, one part of it -- e.g. to emulate the split on one GPU).
+
+    Each rank expands only the node pairs whose ancestor pair at tree level
+    `split_level` hashes to it (gdist.h GdConfig.split_*), and the exact
+    per-rank answers are combined with the reference's witness rule.  The
+    returned QueryResult carries the global distance / witness and this
+    rank's own iteration statistics."""
+    import torch
+
+    from .query import EngineConfig, QueryResult, Witness
+
+    if rank is None or world is None:
+        rank, world = world_info(group)
+    r = split_part(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg or EngineConfig(), rank, world, split_level)
+    w = r.witness
+    mine = torch.tensor([r.distance, -1.0 if w is None else w.tri_a, -1.0 if w is None else w.tri_b,
+                         *(w.point_a if w is not None else np.zeros(3)), *(w.point_b if w is not None else np.zeros(3))],
+                        dtype=torch.float64)
+    dist = _dist()
+    if world > 1 and dist.is_available() and dist.is_initialized() and world == dist.get_world_size(group):
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else mine.device
+        out = torch.empty(world * mine.numel(), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(out, mine.to(dev), group=group)
+        rows = out.cpu().numpy().reshape(world, -1)
+    else:
+        rows = mine.numpy()[None]
+    parts = [(float(x[0]), int(x[1]), int(x[2]), i) for i, x in enumerate(rows)]
+    best = combine_parts(kind, parts)
+    row = rows[best[3]]
+    wit = None if best[1] < 0 else Witness(best[0], best[1], best[2], row[3:6].copy(), row[6:9].copy())
+    return QueryResult(kind, best[0], wit, r.iterations, r.expanded_pairs, r.narrow_pairs, band_pairs=r.band_pairs)
+
+
+def split_part(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank: int, world: int, split_level: int = 5):
+    """This rank's part of a split query: its exact best over the node pairs
+    it owns (QueryResult with the part's own witness and statistics)."""
+    from .query import PreparedQuery
+
+    pq = PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind)
+    pq.g_cfg.split_rank, pq.g_cfg.split_world, pq.g_cfg.split_level = int(rank), int(world), int(split_level)
+    return pq.run()

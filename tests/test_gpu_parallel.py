@@ -1,0 +1,114 @@
+"""Multi-GPU paths on one GPU (gpurun provides one): the split query's parts
+run one after another and combine to the single-GPU answer; two processes
+sharing cuda:0 over a gloo group run the distributed split query and the
+sharded frame sequence end to end."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+SCENES = [("interlocked-rings", {"nu": 100, "nv": 50}), ("interlocked-rings", {"nu": 250, "nv": 100}),
+          ("nested-shells", {"lat": 24, "lon": 30, "r_outer": 0.83}), ("random-blobs", {"n": 3000, "seed": 5}),
+          ("offset-grids", {"res": 30})]
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("scene", range(len(SCENES)))
+def test_split_parts_combine(md, gpu, scene, world):
+    from paper_2411_11244_b200 import parallel
+
+    kind_, params = SCENES[scene]
+    a, b = md.gen_scene(kind_, params)
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    cfg = md.EngineConfig(front_hard_cap=1 << 26)
+    for kind in ("min", "max"):
+        full = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb, cfg)
+        parts = [parallel.split_part(a, b, ta, tb, kind, cfg, r, world) for r in range(world)]
+        rows = [(p.distance, p.witness.tri_a if p.witness else -1, p.witness.tri_b if p.witness else -1, i)
+                for i, p in enumerate(parts)]
+        best = parallel.combine_parts(kind, rows)
+        assert best[0] == full.distance, (kind_, kind, world)
+        assert (best[1], best[2]) == (full.witness.tri_a, full.witness.tri_b)
+        win = parts[best[3]].witness
+        assert win.point_a.tolist() == full.witness.point_a.tolist()
+        # the work is dealt out (each part culls with its own bound, a valid
+        # global bound, so a part far from the optimum may explore a little
+        # more than its share)
+        if full.expanded_pairs > 10_000:
+            assert min(p.expanded_pairs for p in parts) < full.expanded_pairs
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2411_11244_b200 as md
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = md.gen_scene("interlocked-rings", {"nu": 120, "nv": 60})
+        ta, tb = md.build_f12(a), md.build_f12(b)
+        out = {}
+        for kind in ("min", "max"):
+            r = md.run_split_query(a, b, ta, tb, kind)
+            out[kind] = (r.distance, r.witness.tri_a, r.witness.tri_b, r.witness.point_a.tolist())
+        tz, tbase = md.ring_pair_base(60, 30)
+        za, zb = md.build_f12(tz), md.build_f12(tbase)
+        xfs = [md.ring_frame_transforms(f) for f in range(0, 70, 10)]
+        seq = md.run_sequence(tz, tbase, za, zb, xfs, "min")
+        q.put((rank, out, seq.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_gloo(md, gpu):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = []
+    for _ in range(world):
+        try:
+            got.append(q.get(timeout=240))
+        except Exception:
+            for p in procs:
+                p.kill()
+            raise AssertionError(f"worker failed: exit codes {[p.exitcode for p in procs]}")
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    a, b = md.gen_scene("interlocked-rings", {"nu": 120, "nv": 60})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    tz, tbase = md.ring_pair_base(60, 30)
+    za, zb = md.build_f12(tz), md.build_f12(tbase)
+    want_seq = []
+    for f in range(0, 70, 10):
+        xa, xb = md.ring_frame_transforms(f)
+        fa, fb = md.apply_transform(tz, xa), md.apply_transform(tbase, xb)
+        md.refit(za, fa)
+        md.refit(zb, fb)
+        r = md.run_min_query(fa, fb, za, zb)
+        want_seq.append((r.distance, r.witness.tri_a, r.witness.tri_b))
+    for rank, out, seq in got:
+        for kind in ("min", "max"):
+            r = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb)
+            assert out[kind][:3] == (r.distance, r.witness.tri_a, r.witness.tri_b), (rank, kind)
+            assert out[kind][3] == r.witness.point_a.tolist()
+        assert np.array_equal(np.asarray(seq), np.asarray(want_seq, dtype=np.float64)), rank
