@@ -140,6 +140,59 @@ __device__ __forceinline__ T tri_tri_min_d2(const Tri<T>& t1, const Tri<T>& t2, 
   return best;
 }
 
+// The same minimum distance^2 without witness points, features evaluated one
+// at a time (no unrolling): a fraction of the registers, so many more warps
+// per SM hide the float64 latency of the exact pass.  The minimum over the
+// features does not depend on their order, so the value equals
+// tri_tri_min_d2's bit for bit.
+template <typename T>
+__device__ __forceinline__ V3<T> pick3(int i, const V3<T>& a, const V3<T>& b, const V3<T>& c) {
+  return i == 0 ? a : (i == 1 ? b : c);
+}
+template <typename A, typename T>
+__device__ __noinline__ T tri_tri_min_d2_lean(const Tri<T> t1, const Tri<T> t2) {
+  T best = T(INFINITY);
+#pragma unroll 1
+  for (int f = 0; f < 9; ++f) {
+    const int i = f / 3, j = f - 3 * (f / 3);
+    const V3<T> pa = pick3(i, t1.v[0], t1.v[1], t1.v[2]), pa1 = pick3(i == 2 ? 0 : i + 1, t1.v[0], t1.v[1], t1.v[2]);
+    const V3<T> qb = pick3(j, t2.v[0], t2.v[1], t2.v[2]), qb1 = pick3(j == 2 ? 0 : j + 1, t2.v[0], t2.v[1], t2.v[2]);
+    V3<T> p, q;
+    segment_pair<A>(pa, vsub<A>(pa1, pa), qb, vsub<A>(qb1, qb), p, q);
+    const V3<T> w = vsub<A>(p, q);
+    const T d2 = vdot<A>(w, w);
+    best = d2 < best ? d2 : best;
+  }
+#pragma unroll 1
+  for (int f = 0; f < 6; ++f) {
+    const bool a_to_b = (f & 1) == 0;
+    const int i = f >> 1;
+    const Tri<T>& src = a_to_b ? t1 : t2;
+    const Tri<T>& dst = a_to_b ? t2 : t1;
+    const V3<T> p = pick3(i, src.v[0], src.v[1], src.v[2]);
+    const V3<T> q = point_triangle<A>(p, dst.v[0], dst.v[1], dst.v[2]);
+    const V3<T> w = vsub<A>(p, q);
+    const T d2 = vdot<A>(w, w);
+    best = d2 < best ? d2 : best;
+  }
+  if (best > T(0)) {
+#pragma unroll 1
+    for (int f = 0; f < 6; ++f) {
+      const bool a_edge = (f & 1) == 0;
+      const int i = f >> 1;
+      const Tri<T>& e = a_edge ? t1 : t2;
+      const Tri<T>& tr = a_edge ? t2 : t1;
+      V3<T> x;
+      if (pierce<A>(pick3(i, e.v[0], e.v[1], e.v[2]), pick3(i == 2 ? 0 : i + 1, e.v[0], e.v[1], e.v[2]), tr.v[0],
+                    tr.v[1], tr.v[2], x)) {
+        best = T(0);
+        break;
+      }
+    }
+  }
+  return best;
+}
+
 // Exact maximum distance^2 over the 9 vertex pairs, first strict max
 // (bounds.py:309-330)
 template <typename A, typename T, bool kPoints>

@@ -17,12 +17,12 @@ __device__ __forceinline__ Key128 exact_key(const QArgs& q, unsigned ta, unsigne
   if (q.cfg.precision == 32) {
     Tri<float> a = mesh_tri<float>(q.ma, ta), b = mesh_tri<float>(q.mb, tb);
     float d2 = kMax ? tri_tri_max_d2<Exact<float>, float, false>(a, b, nullptr, nullptr)
-                    : tri_tri_min_d2<Exact<float>, float, false>(a, b, nullptr, nullptr);
+                    : tri_tri_min_d2_lean<Exact<float>, float>(a, b);
     d = (double)__fsqrt_rn(d2);
   } else {
     Tri<double> a = mesh_tri<double>(q.ma, ta), b = mesh_tri<double>(q.mb, tb);
     double d2 = kMax ? tri_tri_max_d2<Exact<double>, double, false>(a, b, nullptr, nullptr)
-                     : tri_tri_min_d2<Exact<double>, double, false>(a, b, nullptr, nullptr);
+                     : tri_tri_min_d2_lean<Exact<double>, double>(a, b);
     d = __dsqrt_rn(d2);
   }
   unsigned long long bits = (unsigned long long)__double_as_longlong(d);
@@ -271,7 +271,7 @@ __global__ __launch_bounds__(256) void k_bandsel(QArgs q) {
 constexpr int kRefineThreads = 64;
 
 template <bool kMax>
-__global__ __launch_bounds__(kRefineThreads) void k_refine(QArgs q) {
+__global__ __launch_bounds__(kRefineThreads, 12) void k_refine(QArgs q) {
   QState* S = q.S;
   const unsigned long long n = min(S->n_sel, q.cap);
   const uint2* sel = q.node[S->leaf_buf];

@@ -35,7 +35,7 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static WsLayout ws_layout(const GdConfig& cfg) {
   WsLayout L;
   L.cap = (unsigned long long)std::max<int64_t>(cfg.front_hard_cap, 4);
-  L.band_cap = cfg.band_cap > 0 ? (unsigned long long)cfg.band_cap : (1ull << 20);
+  L.band_cap = cfg.band_cap > 0 ? (unsigned long long)cfg.band_cap : (1ull << 24);  // 200 MB: dense near-contact scenes
   size_t o = 0;
   auto take = [&](size_t& field, size_t bytes) {
     field = o;
@@ -138,7 +138,7 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
   mark(3);
   k_nfilter<kMax, true><<<sms * 8, 256, 0, s>>>(q);  // exits at once unless the band overflowed
   k_bandsel<kMax><<<sms, 256, 0, s>>>(q);
-  k_refine<kMax><<<sms * 4, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
+  k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
   mark(4);
   mark(5);
   GD_CUDA(cudaGetLastError());
