@@ -262,11 +262,16 @@ def run_ours(args):
     hbm, sm_max, src = peaks()
     expand_ms = phases["expand"]
     achieved = qb["expand_bytes"] / (expand_ms * 1e-3) / 1e9 if expand_ms > 0 else None
-    roofline = {"bound": "hbm", "kernel": "k_expand (all iterations of one query)", "achieved": achieved,
-                "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None, "traffic": None,
-                "peak_source": src, "algorithmic_bytes": qb["expand_bytes"], "kernel_ms": expand_ms}
-    narrow_tflops = qb["narrow_flops"] / (phases["narrow"] * 1e-3) / 1e12 if phases["narrow"] > 0 else None
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    traffic = None
+    tf = REPO / "profiles" / "kernel_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text())["per_launch_dram_bytes"].get("k_traverse")
+    roofline = {"bound": "hbm", "kernel": "k_traverse (all expansion iterations of one query, one launch)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
+                "traffic": traffic, "peak_source": src, "algorithmic_bytes": qb["expand_bytes"],
+                "kernel_ms": expand_ms,
+                "note": "algorithmic bytes (SURVEY 8d) count every box load; most hit L2 (traffic = ncu DRAM "
+                        "bytes of one launch, profiles/kernel_traffic.json)"}
 
     # e2e through the public API, per frame: apply_transform A/B + refit A/B
     # (the frame's transforms go host -> device as kernel parameters) +
@@ -332,8 +337,6 @@ def run_ours(args):
             "band_pairs": res.band_pairs,
             "peak_front": res.peak_front,
             "roofline": roofline,
-            "narrow_fp32": {"achieved_tflops": narrow_tflops, "peak_tflops_nominal": fp32_peak,
-                            "frac": (narrow_tflops / fp32_peak) if narrow_tflops else None},
             "e2e": {"value": round(e2e_step_ms / N, 6), "unit": "ms/query", "h2d_bytes_per_step": 2 * 96,
                     "d2h_bytes_per_step": C.sizeof(_lib.GdResult) + 64 * C.sizeof(_lib.GdIterStat),
                     "note": "public API per frame (host wall clock): apply_transform x2 + refit x2 + "
