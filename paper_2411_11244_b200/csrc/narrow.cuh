@@ -58,6 +58,21 @@ __device__ __forceinline__ float axis_gap_sq(const Tri<float>& a, const Tri<floa
   return g > 0.f ? g * g / n2 : 0.f;
 }
 
+// axis_gap_sq(a, b) > ub2 without the division: gap * |n| = bmin - amax along
+// n = (sum of b) - (sum of a); gap^2 > ub2  <=>  (gap |n|)^2 > ub2 |n|^2.
+__device__ __forceinline__ bool axis_separated(const Tri<float>& a, const Tri<float>& b, const V3<float>& sa,
+                                               const V3<float>& sb, float ub2) {
+  const float nx = sb.x - sa.x, ny = sb.y - sa.y, nz = sb.z - sa.z;
+  float amax = -INFINITY, bmin = INFINITY;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    amax = fmaxf(amax, fmaf(a.v[i].x, nx, fmaf(a.v[i].y, ny, a.v[i].z * nz)));
+    bmin = fminf(bmin, fmaf(b.v[i].x, nx, fmaf(b.v[i].y, ny, b.v[i].z * nz)));
+  }
+  const float g = bmin - amax;
+  return g > 0.f && g * g > ub2 * fmaf(nx, nx, fmaf(ny, ny, nz * nz));
+}
+
 // ---------------------------------------------------------------------------
 // Narrow phase, stage 1 (k_nfilter): one thread per leaf pair.  Re-culls the
 // pair with the final traversal bound, loads its 1..2 x 1..2 triangles once (two
@@ -102,13 +117,25 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
       tb[0] = leaf_tri32(q.B, xb, rb, 0);
       if (ca > 1) ta[1] = leaf_tri32(q.A, xa, ra, 1);
       if (cb > 1) tb[1] = leaf_tri32(q.B, xb, rb, 1);
+      // per-triangle quantities once, not per pair
+      Box ba[2], bb[2];
+      V3<float> sa[2], sb[2];  // vertex sums (3 x centroid)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        ba[t] = tri_box(ta[t]);
+        bb[t] = tri_box(tb[t]);
+        sa[t] = {ta[t].v[0].x + ta[t].v[1].x + ta[t].v[2].x, ta[t].v[0].y + ta[t].v[1].y + ta[t].v[2].y,
+                 ta[t].v[0].z + ta[t].v[1].z + ta[t].v[2].z};
+        sb[t] = {tb[t].v[0].x + tb[t].v[1].x + tb[t].v[2].x, tb[t].v[0].y + tb[t].v[1].y + tb[t].v[2].y,
+                 tb[t].v[0].z + tb[t].v[1].z + tb[t].v[2].z};
+      }
 #pragma unroll
       for (int ia = 0; ia < 2; ++ia)
 #pragma unroll
         for (int ib = 0; ib < 2; ++ib) {
           if (ia >= ca || ib >= cb) continue;
-          bool keep = !culling || survives<kMax>(pair_key<kMax>(tri_box(ta[ia]), tri_box(tb[ib])), ub2);
-          if (!kMax && culling && keep) keep = axis_gap_sq(ta[ia], tb[ib]) <= ub2;
+          bool keep = !culling || survives<kMax>(pair_key<kMax>(ba[ia], bb[ib]), ub2);
+          if (!kMax && culling && keep) keep = !axis_separated(ta[ia], tb[ib], sa[ia], sb[ib], ub2);
           if (!keep) continue;
           if (kMax || kRescan) {
             const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr))

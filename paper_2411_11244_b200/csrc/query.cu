@@ -136,7 +136,7 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
   k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
   if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
   mark(3);
-  k_nfilter<kMax, true><<<sms * 8, 256, 0, s>>>(q);  // exits at once unless the band overflowed
+  k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
   k_bandsel<kMax><<<sms, 256, 0, s>>>(q);
   k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
   mark(4);
