@@ -227,6 +227,14 @@ int gd_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const G
 int gd_query_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                    const GdConfig* cfg, void* workspace, size_t workspace_bytes,
                    GdResult* result_dev, void* stream);
+/* gd_query_async that also records `traversal_done` (a cudaEvent_t, may be
+ * NULL) on `stream` right after the traversal kernel: the node boxes are
+ * read by the traversal only, so a refit of these trees for the next frame
+ * may run on another stream once the event fires, overlapping this query's
+ * narrow and exact phases (frame pipelining). */
+int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                      const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
+                      void* stream, void* traversal_done);
 int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* workspace,
                      const GdResult* result_dev, GdResult* out, GdIterStat* stats, int max_stats,
                      void* stream);

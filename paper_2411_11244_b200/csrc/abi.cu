@@ -27,7 +27,7 @@ void export_boxes(const GdMesh& m, const GdBvh& B, int precision, void* nmin, vo
 void pair_greedy(const double* sa, int64_t n, uint8_t* is_left);
 size_t query_workspace_size(const GdConfig& cfg);
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
-                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s);
+                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done);
 void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, GdResult* out, GdIterStat* stats,
                    int max_stats, cudaStream_t s);
 void tri_tri_batch(int kind, int precision, const void* t1, const void* t2, int64_t n, void* d, void* p, void* q,
@@ -170,7 +170,7 @@ int gd_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const G
              void* stream) {
   return guarded([&] {
     GD_CHECK(mesh_a && mesh_b && a && b && cfg && out, GD_ERR_INVALID, "null argument");
-    query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream));
+    query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), nullptr);
     query_collect(*cfg, workspace, nullptr, out, stats, max_stats, S(stream));
     if (out->status == GD_ERR_FRONT_OVERFLOW)
       throw Failure{GD_ERR_FRONT_OVERFLOW, "front expansion would create " + std::to_string(out->overflow_candidates) +
@@ -184,7 +184,17 @@ int gd_query_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, c
                    void* workspace, size_t workspace_bytes, GdResult* result_dev, void* stream) {
   return guarded([&] {
     GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
-    query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream));
+    query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream), nullptr);
+  });
+}
+
+int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                      const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
+                      void* stream, void* traversal_done) {
+  return guarded([&] {
+    GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
+    query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream),
+                static_cast<cudaEvent_t>(traversal_done));
   });
 }
 

@@ -105,7 +105,7 @@ int phase_ms(float* out, int n) {
 }
 
 template <bool kMax>
-static void launch_query(const QArgs& q, cudaStream_t s) {
+static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_done) {
   const int sms = num_sms();
   auto mark = [&](int i) {
     if (g_profile) GD_CUDA(cudaEventRecord(g_ev[i], s));
@@ -132,6 +132,9 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
     GD_CUDA(cudaLaunchCooperativeKernel((const void*)k_traverse<kMax>, dim3(grid[kMax]), dim3(kExpandThreads), args,
                                         kExpandDynSmem, s));
   }
+  // the node boxes are read by k_traverse only: a refit for the next frame
+  // may start once this event has fired
+  if (traversal_done) GD_CUDA(cudaEventRecord(traversal_done, s));
   mark(2);
   k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
   if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
@@ -146,7 +149,7 @@ static void launch_query(const QArgs& q, cudaStream_t s) {
 }
 
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
-                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s) {
+                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done) {
   validate(a, b, cfg);
   WsLayout L = ws_layout(cfg);
   GD_CHECK(ws != nullptr && ws_bytes >= L.total, GD_ERR_WORKSPACE,
@@ -173,9 +176,9 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   q.result = result_dev;  // nullptr: the record stays in the state block (QState::res)
   if (g_profile) g_last_state = q.S;
   if (cfg.kind == 1)
-    launch_query<true>(q, s);
+    launch_query<true>(q, s, traversal_done);
   else
-    launch_query<false>(q, s);
+    launch_query<false>(q, s, traversal_done);
 }
 
 static_assert(offsetof(QState, stats) == offsetof(QState, res) + sizeof(GdResult),

@@ -83,29 +83,75 @@ def run_frames(n_frames: int, frame_fn, group=None, device=None) -> np.ndarray:
     return gather_frames(n_frames, local, group, device)
 
 
-def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cfg=None, group=None) -> np.ndarray:
+def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cfg=None, group=None,
+                 pipelined: bool = True) -> np.ndarray:
     """Distance over a rigid-motion sequence, frames sharded over the ranks.
 
     transforms: list of (xf_a, xf_b) RigidTransform pairs (either may be
     None = identity).  Every rank holds both meshes and trees; returns the
-    (n_frames, 3) array of (distance, tri_a, tri_b) on every rank."""
+    (n_frames, 3) array of (distance, tri_a, tri_b) on every rank.
+
+    pipelined: the refit of frame f+1 runs on a second stream as soon as
+    frame f's traversal has read the boxes (gd_query_async_ev), overlapping
+    frame f's narrow and exact phases."""
+    import torch
+
     from .bvh import refit
     from .mesh import apply_transform
-    from .query import run_max_query, run_min_query
+    from .query import EngineConfig, _plan
 
-    run = run_min_query if kind == "min" else run_max_query
+    cfg = cfg or EngineConfig()
+    rank, world = world_info(group)
+    mine = list(frames_of_rank(len(transforms), rank, world))
 
-    def frame(f):
+    def moved(f):
         xa, xb = transforms[f]
-        a = mesh_a if xa is None else apply_transform(mesh_a, xa)
-        b = mesh_b if xb is None else apply_transform(mesh_b, xb)
-        refit(bvh_a, a)
-        refit(bvh_b, b)
-        r = run(a, b, bvh_a, bvh_b, cfg)
+        return (mesh_a if xa is None else apply_transform(mesh_a, xa),
+                mesh_b if xb is None else apply_transform(mesh_b, xb))
+
+    def row(r):
         w = r.witness
         return r.distance, (-1 if w is None else w.tri_a), (-1 if w is None else w.tri_b)
 
-    return run_frames(len(transforms), frame, group)
+    local = {}
+    if not pipelined or not mine:
+        for f in mine:
+            a, b = moved(f)
+            refit(bvh_a, a)
+            refit(bvh_b, b)
+            pq = _plan(a, b, bvh_a, bvh_b, cfg, kind, None)
+            local[f] = row(pq.run())
+        return gather_frames(len(transforms), local, group)
+    qs = torch.cuda.current_stream()
+    rs = torch.cuda.Stream()
+    trav = torch.cuda.Event()
+    rs.wait_stream(qs)
+
+    def refit_on_rs(a, b, after=None):
+        with torch.cuda.stream(rs):
+            if after is not None:
+                rs.wait_event(after)
+            refit(bvh_a, a)
+            refit(bvh_b, b)
+            done = torch.cuda.Event()
+            done.record(rs)
+        return done
+
+    cur = moved(mine[0])
+    done = refit_on_rs(*cur)
+    for i, f in enumerate(mine):
+        qs.wait_event(done)
+        pq = _plan(cur[0], cur[1], bvh_a, bvh_b, cfg, kind, None)
+        trav = torch.cuda.Event()
+        pq.launch(traversal_done=trav)
+        if i + 1 < len(mine):
+            nxt = moved(mine[i + 1])
+            done = refit_on_rs(*nxt, after=trav)
+        local[f] = row(pq.collect())
+        if i + 1 < len(mine):
+            cur = nxt
+    qs.wait_stream(rs)
+    return gather_frames(len(transforms), local, group)
 
 
 def combine_parts(kind: str, parts: list) -> tuple:

@@ -316,10 +316,19 @@ class PreparedQuery:
         self.g_a, self.g_b = bvh_a.device_view(), bvh_b.device_view()
         return self
 
-    def launch(self, stream=None):
-        _lib.check(_lib.lib().gd_query_async(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a),
-                                             C.byref(self.g_b), C.byref(self.g_cfg), _lib.ptr(self.ws),
-                                             self.ws.numel(), None, stream or _lib.stream_ptr()), "query")
+    def launch(self, stream=None, traversal_done=None):
+        """Enqueue the query on `stream` (default: the current stream).
+        `traversal_done` (a torch.cuda.Event) is recorded right after the
+        traversal: the trees' boxes may be refit for the next frame once it
+        fires (gd_query_async_ev)."""
+        ev = None
+        if traversal_done is not None:
+            if not traversal_done.cuda_event:  # torch creates the event lazily
+                traversal_done.record()
+            ev = C.c_void_p(traversal_done.cuda_event)
+        _lib.check(_lib.lib().gd_query_async_ev(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a),
+                                                C.byref(self.g_b), C.byref(self.g_cfg), _lib.ptr(self.ws),
+                                                self.ws.numel(), None, stream or _lib.stream_ptr(), ev), "query")
 
     def collect(self, stream=None) -> QueryResult:
         _lib.check(_lib.lib().gd_query_collect(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg),
