@@ -235,6 +235,12 @@ int gd_query_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, c
 int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                       const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
                       void* stream, void* traversal_done);
+/* Enqueue the device->host copy of the result record followed by
+ * min(max_stats, 64) GdIterStat into host_dst (pinned memory of at least
+ * sizeof(GdResult) + max_stats * sizeof(GdIterStat) bytes) on `stream`;
+ * the caller synchronises (e.g. an event).  Lets several queries, each with
+ * its own workspace, be in flight. */
+int gd_query_result_async(const GdConfig* cfg, void* workspace, void* host_dst, int max_stats, void* stream);
 int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* workspace,
                      const GdResult* result_dev, GdResult* out, GdIterStat* stats, int max_stats,
                      void* stream);

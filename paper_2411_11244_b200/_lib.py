@@ -144,6 +144,7 @@ _SIGNATURES = {
                                  C.POINTER(GdConfig), P, C.c_size_t, P, P]),
     "gd_query_async_ev": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
                                     C.POINTER(GdConfig), P, C.c_size_t, P, P, P]),
+    "gd_query_result_async": (C.c_int, [C.POINTER(GdConfig), P, P, C.c_int, P]),
     "gd_query_collect": (C.c_int, [C.POINTER(GdBvh), C.POINTER(GdBvh), C.POINTER(GdConfig), P, P,
                                    C.POINTER(GdResult), C.POINTER(GdIterStat), C.c_int, P]),
     "gd_tri_tri_batch": (C.c_int, [C.c_int, C.c_int, P, P, C.c_int64, P, P, P, P]),

@@ -28,6 +28,7 @@ void pair_greedy(const double* sa, int64_t n, uint8_t* is_left);
 size_t query_workspace_size(const GdConfig& cfg);
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done);
+void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
 void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, GdResult* out, GdIterStat* stats,
                    int max_stats, cudaStream_t s);
 void tri_tri_batch(int kind, int precision, const void* t1, const void* t2, int64_t n, void* d, void* p, void* q,
@@ -195,6 +196,13 @@ int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a
     GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
     query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream),
                 static_cast<cudaEvent_t>(traversal_done));
+  });
+}
+
+int gd_query_result_async(const GdConfig* cfg, void* workspace, void* host_dst, int max_stats, void* stream) {
+  return guarded([&] {
+    GD_CHECK(cfg && workspace && host_dst, GD_ERR_INVALID, "null argument");
+    query_result_async(*cfg, workspace, host_dst, max_stats, S(stream));
   });
 }
 

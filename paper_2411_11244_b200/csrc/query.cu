@@ -184,6 +184,15 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
 static_assert(offsetof(QState, stats) == offsetof(QState, res) + sizeof(GdResult),
               "result record and stats must be contiguous (one device->host copy)");
 
+// enqueue the result record + stats copy into caller-provided (pinned) host
+// memory; the caller synchronises (event) -- lets several queries be in flight
+void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s) {
+  WsLayout L = ws_layout(cfg);
+  const QState* S = reinterpret_cast<const QState*>(static_cast<char*>(ws) + L.state);
+  const int ns = std::min(std::max(max_stats, 0), kMaxIters);
+  GD_CUDA(cudaMemcpyAsync(host_dst, &S->res, sizeof(GdResult) + sizeof(GdIterStat) * ns, cudaMemcpyDeviceToHost, s));
+}
+
 // pinned staging for the single device->host copy of result + stats
 static thread_local char* g_pinned = nullptr;
 

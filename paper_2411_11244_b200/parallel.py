@@ -98,7 +98,7 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
 
     from .bvh import refit
     from .mesh import apply_transform
-    from .query import EngineConfig, _plan
+    from .query import EngineConfig, _plan  # noqa: F401  (_plan: unpipelined path)
 
     cfg = cfg or EngineConfig()
     rank, world = world_info(group)
@@ -122,9 +122,13 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
             pq = _plan(a, b, bvh_a, bvh_b, cfg, kind, None)
             local[f] = row(pq.run())
         return gather_frames(len(transforms), local, group)
+    # two query plans with their own workspaces: frame i's query is launched
+    # before frame i-1's result is read, and frame i+1's refit (second stream)
+    # starts as soon as frame i's traversal has read the boxes
+    from .query import PreparedQuery
+
     qs = torch.cuda.current_stream()
     rs = torch.cuda.Stream()
-    trav = torch.cuda.Event()
     rs.wait_stream(qs)
 
     def refit_on_rs(a, b, after=None):
@@ -139,17 +143,23 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
 
     cur = moved(mine[0])
     done = refit_on_rs(*cur)
+    qs.wait_event(done)
+    plans = [PreparedQuery(cur[0], cur[1], bvh_a, bvh_b, cfg, kind, private_workspace=True) for _ in range(2)]
+    pending = None
     for i, f in enumerate(mine):
-        qs.wait_event(done)
-        pq = _plan(cur[0], cur[1], bvh_a, bvh_b, cfg, kind, None)
+        if i:
+            qs.wait_event(done)
+        pq = plans[i % 2].bind(*cur)
         trav = torch.cuda.Event()
-        pq.launch(traversal_done=trav)
+        pq.launch_fetch(traversal_done=trav)
         if i + 1 < len(mine):
             nxt = moved(mine[i + 1])
             done = refit_on_rs(*nxt, after=trav)
-        local[f] = row(pq.collect())
-        if i + 1 < len(mine):
             cur = nxt
+        if pending is not None:
+            local[pending[0]] = row(pending[1].fetch())
+        pending = (f, pq)
+    local[pending[0]] = row(pending[1].fetch())
     qs.wait_stream(rs)
     return gather_frames(len(transforms), local, group)
 

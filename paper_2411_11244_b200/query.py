@@ -287,8 +287,10 @@ class PreparedQuery:
     (frames, benches) cost only the kernel sequence.  `launch()` is
     asynchronous; `collect()` does the single device->host copy."""
 
-    def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, cfg: EngineConfig, kind: str, warm_pair=None):
+    def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, cfg: EngineConfig, kind: str, warm_pair=None,
+                 private_workspace: bool = False):
         _check_build(cfg, bvh_a, bvh_b)
+        self._pinned = self._ready = None
         self.kind = kind
         self.warm_pair = warm_pair
         self.trees = (bvh_a, bvh_b)
@@ -298,7 +300,7 @@ class PreparedQuery:
         L = _lib.lib()
         _lib.check(L.gd_query_workspace_size(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg),
                                              C.byref(nbytes)), "query_workspace_size")
-        self.ws = _Workspace.get(nbytes.value)
+        self.ws = _lib.empty(nbytes.value, _lib.torch().uint8) if private_workspace else _Workspace.get(nbytes.value)
         self.res = _lib.GdResult()
         self.stats = (_lib.GdIterStat * _MAX_STATS)()
 
@@ -339,6 +341,30 @@ class PreparedQuery:
     def run(self) -> QueryResult:
         self.launch()
         return self.collect()
+
+    # -- several queries in flight (each PreparedQuery with its own workspace)
+    def launch_fetch(self, stream=None, traversal_done=None):
+        """launch() + an asynchronous copy of the result record and stats to
+        pinned host memory; `fetch()` waits for it.  The query's workspace
+        is busy until fetch() returns."""
+        torch = _lib.torch()
+        if self._pinned is None:
+            n = C.sizeof(_lib.GdResult) + _MAX_STATS * C.sizeof(_lib.GdIterStat)
+            self._pinned = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+            self._ready = torch.cuda.Event()
+        self.launch(stream, traversal_done)
+        s = stream or _lib.stream_ptr()
+        _lib.check(_lib.lib().gd_query_result_async(C.byref(self.g_cfg), _lib.ptr(self.ws), _lib.ptr(self._pinned),
+                                                    _MAX_STATS, s), "query_result_async")
+        self._ready.record()
+        return self
+
+    def fetch(self) -> QueryResult:
+        self._ready.synchronize()
+        base = self._pinned.data_ptr()
+        r = _lib.GdResult.from_address(base)
+        stats = (_lib.GdIterStat * _MAX_STATS).from_address(base + C.sizeof(_lib.GdResult))
+        return _result(self.kind, r, stats)
 
 
 # recently used query plans, keyed by (trees, config, kind, warm pair, device);
