@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 6
+#define GDIST_ABI_VERSION 7
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -89,11 +89,8 @@ typedef struct GdBvhSizes {
  *              counter, then the refit's subtree arrival counters
  *   leaf_xvtx: 2 * L float4 (capacity): the 5th and 6th distinct vertex
  *              (repeated when only five) of each masked leaf, by rank
- *   leaf_pat : L uint32: the leaf's triangles in its distinct-vertex list --
- *              triangle 0 is (0, 1, 2); bits 0-8 hold triangle 1's three
- *              3-bit indices, bit 9 is set when the leaf has two triangles
- * leaf_vtx, leaf_x, leaf_xvtx and leaf_pat are written by
- * gd_stage_vertices; the refit and the narrow filter stream them. */
+ * leaf_vtx, leaf_x and leaf_xvtx are written by gd_stage_vertices; the
+ * refit streams them. */
 typedef struct GdBvh {
   float* box;
   int32_t* leaf_rec;
@@ -102,7 +99,6 @@ typedef struct GdBvh {
   float* leaf_vtx;
   uint32_t* leaf_x;
   float* leaf_xvtx;
-  uint32_t* leaf_pat;
   int64_t leaf_count;
   int64_t n_tris;
   int64_t nv;

@@ -60,7 +60,6 @@ class GdBvh(C.Structure):
         ("leaf_vtx", C.c_void_p),
         ("leaf_x", C.c_void_p),
         ("leaf_xvtx", C.c_void_p),
-        ("leaf_pat", C.c_void_p),
         ("leaf_count", C.c_int64),
         ("n_tris", C.c_int64),
         ("nv", C.c_int64),

@@ -148,52 +148,6 @@ __device__ __forceinline__ Tri<float> leaf_tri32(const GdBvh& T, const XfF32& x,
   return i ? tri32(T, x, r.r0.w, r.r1.x, r.r1.y) : tri32(T, x, r.r0.x, r.r0.y, r.r0.z);
 }
 
-// A leaf's triangles from its streamed distinct-vertex set (gdist.h
-// leaf_vtx / leaf_x / leaf_xvtx / leaf_pat): three coalescable float4 plane
-// loads + one pattern word, the extras only for the rare 5-6-vertex leaves --
-// no index gathers.  Same xf_apply as the refit, so the boxes contain
-// exactly these vertices.
-__device__ __forceinline__ V3<float> pick6(unsigned i, const V3<float>* v) {
-  V3<float> r = v[0];
-#pragma unroll
-  for (int j = 1; j < 6; ++j)
-    if (i == (unsigned)j) r = v[j];
-  return r;
-}
-__device__ __forceinline__ int leaf_geo(const GdBvh& T, const XfF32& x, unsigned l, Tri<float>& t0,
-                                        Tri<float>& t1) {
-  const unsigned L = (unsigned)T.leaf_count;
-  const float4* p = reinterpret_cast<const float4*>(T.leaf_vtx);
-  const float4 a = __ldg(p + l), b = __ldg(p + L + l), c = __ldg(p + 2 * L + l);
-  const unsigned pat = __ldg(T.leaf_pat + l);
-  V3<float> v[6];
-  v[0] = xf_apply(x, make_float4(a.x, a.y, a.z, 0.f));
-  v[1] = xf_apply(x, make_float4(a.w, b.x, b.y, 0.f));
-  v[2] = xf_apply(x, make_float4(b.z, b.w, c.x, 0.f));
-  v[3] = xf_apply(x, make_float4(c.y, c.z, c.w, 0.f));
-  t0.v[0] = v[0];
-  t0.v[1] = v[1];
-  t0.v[2] = v[2];
-  if (!((pat >> 9) & 1u)) {
-    t1 = t0;
-    return 1;
-  }
-  const unsigned i0 = pat & 7u, i1 = (pat >> 3) & 7u, i2 = (pat >> 6) & 7u;
-  v[4] = v[5] = v[0];
-  if ((i0 | i1 | i2) & 4u) {  // uses a 5th / 6th distinct vertex
-    const unsigned W = (L + 31) >> 5, bit = l & 31u;
-    const unsigned mask = __ldg(T.leaf_x + (l >> 5));
-    const unsigned rank = __ldg(T.leaf_x + W + (l >> 5)) + __popc(mask & ((1u << bit) - 1));
-    const float4* xv = reinterpret_cast<const float4*>(T.leaf_xvtx);
-    v[4] = xf_apply(x, __ldg(xv + 2 * rank));
-    v[5] = xf_apply(x, __ldg(xv + 2 * rank + 1));
-  }
-  t1.v[0] = pick6(i0, v);
-  t1.v[1] = pick6(i1, v);
-  t1.v[2] = pick6(i2, v);
-  return 2;
-}
-
 __device__ __forceinline__ Box tri_box(const Tri<float>& t) {
   Box b;
   b.lo[0] = fminf(fminf(t.v[0].x, t.v[1].x), t.v[2].x);

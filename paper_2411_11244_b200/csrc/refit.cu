@@ -197,18 +197,6 @@ __global__ __launch_bounds__(256) void k_leaf_vtx(GdBvh T) {
       if (!seen) u[k++] = s[i];
     }
     for (int i = k; i < 6; ++i) u[i] = u[0];
-    // triangle 1 in the distinct list (triangle 0 is always (0, 1, 2): a
-    // triangle has three distinct vertices, mesh.py:32-58)
-    unsigned pat = r.count() > 1 ? (1u << 9) : 0u;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      int idx = 0;
-#pragma unroll
-      for (int j = 5; j >= 0; --j)
-        if (j < k && u[j] == s[3 + c]) idx = j;
-      pat |= (unsigned)idx << (3 * c);
-    }
-    T.leaf_pat[l] = pat;
     const float4* v = reinterpret_cast<const float4*>(T.vtx32);
     const float4 a = v[u[0]], b = v[u[1]], c = v[u[2]], d = v[u[3]];
     float4* p = reinterpret_cast<float4*>(T.leaf_vtx);
@@ -238,8 +226,7 @@ __global__ __launch_bounds__(256) void k_leaf_vtx(GdBvh T) {
 
 void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "mesh vertex count differs from the tree's");
-  GD_CHECK(T.leaf_vtx && T.leaf_x && T.leaf_xvtx && T.leaf_pat, GD_ERR_INVALID,
-           "GdBvh leaf vertex sets must be allocated");
+  GD_CHECK(T.leaf_vtx && T.leaf_x && T.leaf_xvtx, GD_ERR_INVALID, "GdBvh leaf vertex sets must be allocated");
   if (m.nv > 0)
     k_stage<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, T.vmap, reinterpret_cast<float4*>(T.vtx32));
   const long long W = (T.leaf_count + 31) / 32;

@@ -235,11 +235,7 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
                                              int lb) {
   QState* S = q.S;
   const int shift = ka + kb;
-#ifdef GD_K1_GENERIC
-  const bool k1 = false;
-#else
   const bool k1 = (k == 1);
-#endif
   const unsigned long long tiles = k1 ? (n_in + kK1Tile - 1) / kK1Tile : (ncand + kGenericTile - 1) / kGenericTile;
   const uint2* __restrict__ in_node = q.node[cur];
   const float* __restrict__ in_key = q.key[cur];
