@@ -20,6 +20,8 @@
 namespace gd {
 
 constexpr int kFold = 256;  // nodes per block per fold (8 levels)
+// gdist.h sizes the cascade counters in leaf_x for 256-leaf blocks (2 (L >> 16) + 4)
+static_assert(kFold == 256, "leaf_x cascade counter capacity assumes 256-leaf blocks");
 
 __global__ __launch_bounds__(256) void k_stage(GdMesh m, const int32_t* __restrict__ vmap, float4* __restrict__ out) {
   const long long i = blockIdx.x * 256ll + threadIdx.x;
