@@ -43,7 +43,7 @@ struct alignas(16) QState {
   int band_overflow;
   unsigned bar;                      // grid-barrier arrivals (k_traverse)
   unsigned fbest;                    // best float32 narrow distance (ordered bits)
-  unsigned long long cnt[kMaxIters + 1];       // survivors written by iteration i
+  unsigned long long cnt[kMaxIters + 1];       // iteration i: survivors (low 40 bits) + arrivals
   unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
   unsigned long long skip_it[kMaxIters];       // candidates of pairs another split rank owns
   GdResult res;                      // the result record, then the stats: one

@@ -207,6 +207,27 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 // release-arrive / acquire-spin: every block's writes before the barrier are
 // visible to every block after it.  Data written in the same launch (fronts,
 // counters) is read with plain coherent loads, never through __ldg.
+// Iteration barrier fused with the survivor count: cnt[it] holds the
+// survivors (low 40 bits, reserved by the tiles with plain atomicAdd) and the
+// block arrivals (high 24 bits).  Returns the final survivor count -- no
+// separate load after the barrier.
+constexpr int kArriveShift = 40;
+__device__ __forceinline__ unsigned long long count_barrier(unsigned long long* cnt) {
+  __shared__ unsigned long long total;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long target = (unsigned long long)gridDim.x << kArriveShift;
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(cnt), "l"(1ull << kArriveShift) : "memory");
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+    } while ((v & ~((1ull << kArriveShift) - 1)) < target);
+    total = v & ((1ull << kArriveShift) - 1);
+  }
+  __syncthreads();
+  return total;
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -271,8 +292,8 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
       const unsigned long long e0 = t0 + threadIdx.x;
       float pk_next = e0 < t1 ? in_key[e0] : 0.f;
       uint2 nd_next = e0 < t1 ? in_node[e0] : make_uint2(0, 0);
-      __syncthreads();
       const float ub = load_bound_sq(S);  // one bound snapshot per tile (query.py:396)
+      __syncthreads();
       float upd = kMax ? 0.f : INFINITY;
 #pragma unroll 1
       for (int r = 0; r < R; ++r) {
@@ -362,7 +383,9 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
       __syncthreads();
       if (threadIdx.x == 0) {
         const unsigned total = sh.stage_count;
-        sh.out_base = total ? atomicAdd(n_out, (unsigned long long)total) : 0ull;
+        // low 40 bits: survivors so far (blocks that finished have added their
+        // arrival in the high bits, count_barrier)
+        sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
         float u = sh.warp_upd[0];
         for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
         if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
@@ -425,7 +448,9 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
       if ((threadIdx.x & 31) == 0) sh.warp_upd[threadIdx.x >> 5] = upd;
       __syncthreads();
       if (threadIdx.x == 0) {
-        sh.out_base = total ? atomicAdd(n_out, (unsigned long long)total) : 0ull;
+        // low 40 bits: survivors so far (blocks that finished have added their
+        // arrival in the high bits, count_barrier)
+        sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
         float u = sh.warp_upd[0];
         for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
         if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
@@ -499,8 +524,7 @@ __global__ __launch_bounds__(kExpandThreads, 4) void k_traverse(QArgs q) {
     }
     expand_sweep<kMax>(q, sh, k1_stage, it, cur, n_in, k, ka, kb, to_leaves, ncand, da, db, la, lb);
     if (q.profile && threadIdx.x == 0) atomicMax(&S->t_sweep[it], globaltimer_ns());
-    grid_barrier(&S->bar, ++phase);
-    const unsigned long long n_out = V->cnt[it];
+    const unsigned long long n_out = count_barrier(&S->cnt[it]);
     if (n_out > (unsigned long long)q.cfg.front_hard_cap) {  // query.py:448-449
       if (rec) {
         S->err = GD_ERR_FRONT_OVERFLOW;
