@@ -53,6 +53,11 @@ def parse():
     return ap.parse_args()
 
 
+def workload_name(args):
+    return (f"rings 2 x {args.nu * args.nv * 2} tris (configs 2/3): a step is one frame f = step * N + rank of the "
+            f"1000-frame rotation sequence = refit A + refit B + {args.kind} distance query")
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -346,9 +351,9 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f32 traversal + f64 exact pass",
             "data": "synthetic (interlocked tori, rotation sequence frames)",
-            "config": {"workload": f"rings {2 * args.nu * args.nv} tris/mesh (configs 2/3), frame f = step*N + rank; "
-                                   f"step = refit A + refit B + {args.kind} query of the frame; frames pipelined "
-                                   f"(refit of frame f+1 on a second stream overlaps frame f's narrow/exact phases)",
+            "config": {"workload": workload_name(args),
+                       "execution": "frames pipelined: the refit of frame f+1 runs on a second stream and overlaps "
+                                    "frame f's narrow / exact phases",
                        "nu": args.nu, "nv": args.nv, "kind": args.kind, "precision": 64,
                        "l2": "inputs larger than L2 (2 x 200 MB node boxes rewritten by each step's refits)"},
             "query_ms": round(float(np.mean(query_ms)), 6),
@@ -541,9 +546,9 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (interlocked tori, rotation sequence frames)",
-        "config": {"workload": f"rings {2 * args.nu * args.nv} tris/mesh (config 2), frame f = step*N; step = "
-                               f"refit A + refit B + {args.kind} query", "nu": args.nu, "nv": args.nv,
-                   "kind": args.kind, "precision": 64},
+        "config": {"workload": workload_name(args),
+                   "execution": "frames one after another on the host (the reference's stock, synchronous path)",
+                   "nu": args.nu, "nv": args.nv, "kind": args.kind, "precision": 64},
         "cpu_baseline": {"value": round(value, 3), "unit": "ms/query", "cores": workers, "kind": leg.kind_label,
                          "sample": f"{len(times)} frame steps (bounded to {args.cpu_budget:.0f} s) of the same "
                                    f"workload, {leg.describe()}"},

@@ -241,6 +241,19 @@ int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* 
                      const GdResult* result_dev, GdResult* out, GdIterStat* stats, int max_stats,
                      void* stream);
 
+/* ---- OBJ ingest (mesh.py:112-163 load_obj), host only ------------------ */
+/* Parse a Wavefront OBJ file with the reference's semantics (v / f records,
+ * `#` comments, fan triangulation, negative relative indices, every other
+ * record ignored).  On success *handle owns the mesh (read it with
+ * gd_obj_read into caller buffers of 3 * n_vertices doubles and
+ * 3 * n_triangles int64, then gd_obj_close).  On a malformed record returns
+ * GD_ERR_INVALID with *err_line = its 1-based line and the reference's
+ * message in gd_last_error(); *err_line = 0 means the file could not be
+ * opened. */
+int gd_obj_open(const char* path, void** handle, int64_t* n_vertices, int64_t* n_triangles, int64_t* err_line);
+int gd_obj_read(void* handle, double* vertices, int64_t* triangles);
+void gd_obj_close(void* handle);
+
 /* ---- batch math (bounds.py) ------------------------------------------- */
 /* batch_tri_tri_min / batch_tri_tri_max (bounds.py:245-330), exact
  * reference arithmetic in `precision` (32 / 64).  t1, t2: device (n, 3, 3);

@@ -146,6 +146,10 @@ _SIGNATURES = {
     "gd_query_result_async": (C.c_int, [C.POINTER(GdConfig), P, P, C.c_int, P]),
     "gd_query_collect": (C.c_int, [C.POINTER(GdBvh), C.POINTER(GdBvh), C.POINTER(GdConfig), P, P,
                                    C.POINTER(GdResult), C.POINTER(GdIterStat), C.c_int, P]),
+    "gd_obj_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                              C.POINTER(C.c_int64)]),
+    "gd_obj_read": (C.c_int, [P, P, P]),
+    "gd_obj_close": (None, [P]),
     "gd_tri_tri_batch": (C.c_int, [C.c_int, C.c_int, P, P, C.c_int64, P, P, P, P]),
     "gd_tri_tri_fast": (C.c_int, [C.c_int, P, P, C.c_int64, P, P]),
     "gd_box_bounds_batch": (C.c_int, [C.c_int, C.c_int, P, P, P, P, C.c_int64, P, P]),

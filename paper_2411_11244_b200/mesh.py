@@ -194,42 +194,25 @@ def apply_transform(mesh: TriangleMesh, xf: RigidTransform) -> TriangleMesh:
 
 
 def load_obj(path) -> TriangleMesh:
-    """Wavefront OBJ subset: `v`, `f` (fan-triangulated, negative indices
-    relative), `#` comments; everything else ignored (mesh.py:108-163)."""
+    """Wavefront OBJ subset with the reference's semantics (mesh.py:108-163):
+    `v` and `f` records, `#` comments, polygons fan-triangulated, negative
+    indices relative to the vertex count at the point of use, everything
+    else ignored.  Parsed natively (csrc/obj.cpp, host C++); a malformed
+    record raises ObjParseError(path, line_no, message)."""
     path = os.fspath(path)
-    verts: list = []
-    faces: list = []
-    with open(path, "r", encoding="utf-8", errors="replace") as fh:
-        for line_no, raw in enumerate(fh, start=1):
-            body = raw.split("#", 1)[0].strip()
-            if not body:
-                continue
-            tok = body.split()
-            if tok[0] == "v":
-                if len(tok) < 4:
-                    raise ObjParseError(path, line_no, "vertex needs 3 coordinates")
-                try:
-                    verts.append((float(tok[1]), float(tok[2]), float(tok[3])))
-                except ValueError as exc:
-                    raise ObjParseError(path, line_no, f"bad vertex coordinate: {exc}") from None
-            elif tok[0] == "f":
-                if len(tok) < 4:
-                    raise ObjParseError(path, line_no, "face needs at least 3 vertices")
-                idx = []
-                for item in tok[1:]:
-                    head = item.split("/", 1)[0]
-                    try:
-                        ref = int(head)
-                    except ValueError:
-                        raise ObjParseError(path, line_no, f"bad face index {item!r}") from None
-                    if ref == 0:
-                        raise ObjParseError(path, line_no, "face index 0 is not valid OBJ")
-                    k = ref - 1 if ref > 0 else len(verts) + ref
-                    if k < 0 or k >= len(verts):
-                        raise ObjParseError(path, line_no, f"face index {ref} out of range (have {len(verts)} vertices)")
-                    idx.append(k)
-                faces.extend((idx[0], idx[i], idx[i + 1]) for i in range(1, len(idx) - 1))
-    return TriangleMesh(
-        np.asarray(verts, dtype=np.float64).reshape(len(verts), 3),
-        np.asarray(faces, dtype=np.int64).reshape(len(faces), 3),
-    )
+    L = _lib.lib()
+    h = C.c_void_p()
+    nv, nt, line = C.c_int64(), C.c_int64(), C.c_int64()
+    st = L.gd_obj_open(os.fsencode(path), C.byref(h), C.byref(nv), C.byref(nt), C.byref(line))
+    if st != 0:
+        msg = L.gd_last_error().decode("utf-8", "replace")
+        if line.value == 0:
+            raise OSError(msg)
+        raise ObjParseError(path, int(line.value), msg)
+    try:
+        verts = np.empty((nv.value, 3), dtype=np.float64)
+        tris = np.empty((nt.value, 3), dtype=np.int64)
+        L.gd_obj_read(h, verts.ctypes.data_as(C.c_void_p), tris.ctypes.data_as(C.c_void_p))
+    finally:
+        L.gd_obj_close(h)
+    return TriangleMesh(verts, tris)

@@ -106,3 +106,56 @@ def test_engine_small_tori(reference, oracle, md, kind, prec):
     assert [tuple(s[:4]) for s in got.iterations] == [(s.k, s.front_in, s.front_out, s.culled)
                                                       for s in want.iterations]
     assert got.expanded_pairs == want.expanded_pairs and got.narrow_pairs == want.narrow_pairs
+
+
+OBJ_CASES = [
+    "# comment\nv 0 0 0\nv 1 0 0 # trailing\nv 1 1 0\nv 0 1 0\nvn 0 0 1\nvt 0 0\nf 1/1/1 2/2/1 3//1 4\nf -4 -3 -2\n",
+    "v 1e-3 .5 5.\r\nv +1_0.5 -0 2E+2\r\nv inf 0 -NaN\r\nv 0 0 1\rf 1 2 3\r\ng grp\no obj\ns off\nf 2 3 4 1\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 3\n\n\n   \n\tf -1 -2 -3\nusemtl x\nf 0003 +2 1_0\n",
+    "v 0 0\n",
+    "v 0 0 zero\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 0\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 4\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 -4\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 x/1\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 /3\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 2 99999999999999999999999\n",
+    "v 0 0 0\nv 1 0 0\nv 0 1 0\nf 1 1 2\n",
+    "v 0 0 0\nv 1 0 0\rv 0 1 0\r\nf 1 2 3 'q\n",
+    "",
+]
+
+
+@pytest.mark.parametrize("case", range(len(OBJ_CASES)))
+def test_load_obj_matches_reference(reference, md, tmp_path, case):
+    """The native OBJ parser (csrc/obj.cpp) against the reference's load_obj
+    (mesh.py:112-163): same arrays, or the same exception type, line and
+    message."""
+    p = tmp_path / f"c{case}.obj"
+    p.write_bytes(OBJ_CASES[case].encode())
+    try:
+        want = reference.load_obj(p)
+    except Exception as exc:  # noqa: BLE001 - compare the failure itself
+        with pytest.raises(Exception) as got:
+            md.load_obj(p)
+        assert type(got.value).__name__ == type(exc).__name__
+        assert str(got.value) == str(exc)
+        assert getattr(got.value, "line_no", None) == getattr(exc, "line_no", None)
+        return
+    got = md.load_obj(p)
+    assert np.array_equal(got.vertices, want.vertices, equal_nan=True)
+    assert np.array_equal(got.triangles, want.triangles)
+
+
+def test_load_obj_large_matches_reference(reference, md, tmp_path):
+    """A 20K-triangle OBJ written from a torus: identical arrays."""
+    tz, _ = md.ring_pair_base(100, 100)
+    p = tmp_path / "torus.obj"
+    with open(p, "w") as fh:
+        for v in tz.vertices:
+            fh.write(f"v {float(v[0])!r} {float(v[1])!r} {float(v[2])!r}\n")
+        for t in tz.triangles:
+            fh.write(f"f {t[0] + 1} {t[1] + 1} {t[2] + 1}\n")
+    got, want = md.load_obj(p), reference.load_obj(p)
+    assert np.array_equal(got.vertices, want.vertices) and np.array_equal(got.triangles, want.triangles)
