@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 7
+#define GDIST_ABI_VERSION 8
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -127,7 +127,12 @@ typedef struct GdConfig {
   int32_t split_rank;
   int32_t split_world;       /* 0 or 1 = no split                            */
   int32_t split_level;
-  int32_t _pad;
+  /* traversal frame: 0 = world; 1 = B's local frame -- tree B's boxes are
+   * those of B's untransformed vertices and tree A's those of A under
+   * gd_mesh_relative(A, B), so a sequence where both meshes move refits one
+   * tree per frame.  The exact pass always works in world coordinates, so
+   * the answer is bitwise the world-frame one. */
+  int32_t frame;
 } GdConfig;
 
 /* QueryResult (query.py:230-263) + Witness (query.py:136-144). */
@@ -192,6 +197,11 @@ int gd_bvh_layout(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t worksp
  * into bvh->vtx32 at the slots of bvh->vmap.  Needed once per base vertex
  * buffer. Asynchronous. */
 int gd_stage_vertices(const GdMesh* mesh, GdBvh* bvh, void* stream);
+
+/* *out = *a with the rigid transform of A expressed in B's local frame:
+ * R = Rb^T Ra, t = Rb^T (ta - tb) (float64, fixed operation order; the
+ * transform GdConfig.frame = 1 queries apply to A).  Host only. */
+int gd_mesh_relative(const GdMesh* a, const GdMesh* b, GdMesh* out);
 
 /* refit (bvh.py:292-306) with apply_transform (mesh.py:102-105) fused:
  * leaf boxes of the transformed staged vertices, bottom-up unions.

@@ -38,7 +38,7 @@ from .errors import (
     TightnessError,
     TopologyMismatchError,
 )
-from .mesh import RigidTransform, TriangleMesh, apply_transform, load_obj
+from .mesh import RigidTransform, TriangleMesh, apply_transform, load_obj, relative_mesh
 from .query import (
     EngineConfig,
     Front,
@@ -151,6 +151,7 @@ __all__ = [
     "node_level",
     "process_leaf_pair",
     "refit",
+    "relative_mesh",
     "remaining_depth",
     "ring_frame_transforms",
     "ring_pair_base",

@@ -84,7 +84,7 @@ class GdConfig(C.Structure):
         ("split_rank", C.c_int32),
         ("split_world", C.c_int32),
         ("split_level", C.c_int32),
-        ("_pad", C.c_int32),
+        ("frame", C.c_int32),
     ]
 
 
@@ -131,6 +131,7 @@ _SIGNATURES = {
     "gd_bvh_build": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P, C.c_size_t, P, P, P]),
     "gd_bvh_layout": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P, C.c_size_t, P]),
     "gd_stage_vertices": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P]),
+    "gd_mesh_relative": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdMesh)]),
     "gd_refit": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P]),
     "gd_export_boxes": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), C.c_int, P, P, P]),
     "gd_pair_greedy": (C.c_int, [P, C.c_int64, P]),

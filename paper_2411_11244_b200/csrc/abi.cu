@@ -6,7 +6,7 @@
 #include <atomic>
 #include <string>
 
-#include "common.cuh"
+#include "engine.cuh"
 
 namespace gd {
 
@@ -125,6 +125,13 @@ int gd_bvh_layout(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t worksp
   return guarded([&] {
     GD_CHECK(mesh && bvh, GD_ERR_INVALID, "null argument");
     bvh_layout(*mesh, *bvh, workspace, workspace_bytes, S(stream));
+  });
+}
+
+int gd_mesh_relative(const GdMesh* a, const GdMesh* b, GdMesh* out) {
+  return guarded([&] {
+    GD_CHECK(a && b && out, GD_ERR_INVALID, "null argument");
+    *out = relative_mesh(*a, *b);
   });
 }
 

@@ -15,6 +15,26 @@ struct XfF32 {
   float r[9], t[3];
   int has;
 };
+// A's transform in B's local frame: R = Rb^T Ra, t = Rb^T (ta - tb)
+inline GdMesh relative_mesh(const GdMesh& a, const GdMesh& b) {
+  GdMesh r = a;
+  double Ra[9], ta[3], Rb[9], tb[3];
+  for (int i = 0; i < 9; ++i) {
+    Ra[i] = a.has_xf ? a.rot[i] : (i % 4 == 0 ? 1.0 : 0.0);
+    Rb[i] = b.has_xf ? b.rot[i] : (i % 4 == 0 ? 1.0 : 0.0);
+  }
+  for (int i = 0; i < 3; ++i) {
+    ta[i] = a.has_xf ? a.trans[i] : 0.0;
+    tb[i] = b.has_xf ? b.trans[i] : 0.0;
+  }
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r.rot[3 * i + j] = (Rb[i] * Ra[j] + Rb[3 + i] * Ra[3 + j]) + Rb[6 + i] * Ra[6 + j];
+  for (int i = 0; i < 3; ++i)
+    r.trans[i] = (Rb[i] * (ta[0] - tb[0]) + Rb[3 + i] * (ta[1] - tb[1])) + Rb[6 + i] * (ta[2] - tb[2]);
+  r.has_xf = 1;
+  return r;
+}
+
 // computed once on the host (float64 -> float32 conversions are slow on the
 // device) and passed by value in the kernel arguments
 inline XfF32 xf32_host(const GdMesh& m) {

@@ -61,6 +61,7 @@ static void validate(const GdBvh& a, const GdBvh& b, const GdConfig& cfg) {
   GD_CHECK(cfg.front_cap >= 4, GD_ERR_CONFIG, "front_cap must be >= 4");
   GD_CHECK(cfg.depth_cap >= 1 && cfg.depth_cap <= 16, GD_ERR_CONFIG, "depth_cap must be in [1, 16]");
   GD_CHECK(cfg.front_hard_cap >= 4, GD_ERR_CONFIG, "front_hard_cap must be >= 4");
+  GD_CHECK(cfg.frame == 0 || cfg.frame == 1, GD_ERR_CONFIG, "frame must be 0 (world) or 1 (B-local)");
   GD_CHECK(a.depth >= 0 && a.depth <= 31 && b.depth >= 0 && b.depth <= 31, GD_ERR_INVALID,
            "tree depth out of range");
   GD_CHECK(a.box && b.box && a.leaf_rec && b.leaf_rec && a.vtx32 && b.vtx32 && a.vmap && b.vmap,
@@ -159,8 +160,15 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   q.ma = ma;
   q.mb = mb;
   q.profile = g_profile ? 1 : 0;
-  q.xa = xf32_host(ma);
-  q.xb = xf32_host(mb);
+  if (cfg.frame == 1) {  // traversal in B's local frame (gdist.h GdConfig.frame)
+    q.xa = xf32_host(relative_mesh(ma, mb));
+    GdMesh id = mb;
+    id.has_xf = 0;
+    q.xb = xf32_host(id);
+  } else {
+    q.xa = xf32_host(ma);
+    q.xb = xf32_host(mb);
+  }
   q.A = a;
   q.B = b;
   q.cfg = cfg;

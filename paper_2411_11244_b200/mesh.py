@@ -148,6 +148,19 @@ class TriangleMesh:
         return (id(self._root), self._rot.tobytes() + self._trans.tobytes())
 
 
+def relative_mesh(mesh_a: "TriangleMesh", mesh_b: "TriangleMesh") -> "TriangleMesh":
+    """mesh_a's base geometry under A's transform expressed in B's local
+    frame (Rb^T Ra, Rb^T (ta - tb); gd_mesh_relative, the transform a
+    GdConfig.frame = 1 query applies to A)."""
+    L = _lib.lib()
+    out = _lib.GdMesh()
+    _lib.check(L.gd_mesh_relative(C.byref(mesh_a.device_view()), C.byref(mesh_b.device_view()), C.byref(out)),
+               "mesh_relative")
+    rot = np.array(out.rot[:], dtype=np.float64).reshape(3, 3)
+    trans = np.array(out.trans[:], dtype=np.float64)
+    return TriangleMesh._moved(mesh_a._root, RigidTransform(rot, trans))
+
+
 class RigidTransform:
     """Rotation (3x3 orthonormal within 1e-6) then translation (mesh.py:69-99)."""
 

@@ -84,49 +84,67 @@ def run_frames(n_frames: int, frame_fn, group=None, device=None) -> np.ndarray:
 
 
 def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cfg=None, group=None,
-                 pipelined: bool = True) -> np.ndarray:
+                 pipelined: bool = True, frame: str = "world") -> np.ndarray:
     """Distance over a rigid-motion sequence, frames sharded over the ranks.
 
     transforms: list of (xf_a, xf_b) RigidTransform pairs (either may be
     None = identity).  Every rank holds both meshes and trees; returns the
     (n_frames, 3) array of (distance, tri_a, tri_b) on every rank.
 
-    pipelined: the refit of frame f+1 runs on a second stream as soon as
+    frame: "world" refits both trees per frame.  "b-local" traverses in B's
+    local frame (GdConfig.frame = 1): B's boxes are computed once and only
+    A's tree is refit per frame, under A's transform relative to B -- half
+    the refit work when both meshes move -- but axis-aligned boxes cull
+    differently in another frame: on the rings sequence the B-local
+    traversal is slower than the refit it saves.  The exact pass
+    stays in world coordinates, so the answers are bitwise the world ones.
+    pipelined: the refit for frame f+1 runs on a second stream as soon as
     frame f's traversal has read the boxes (gd_query_async_ev), overlapping
-    frame f's narrow and exact phases."""
+    frame f's narrow and exact phases, and two query plans are in flight so
+    the host never waits on the GPU between frames."""
     import torch
 
     from .bvh import refit
-    from .mesh import apply_transform
-    from .query import EngineConfig, _plan  # noqa: F401  (_plan: unpipelined path)
+    from .mesh import apply_transform, relative_mesh
+    from .query import EngineConfig, PreparedQuery
 
+    if frame not in ("world", "b-local"):
+        raise ValueError(f"frame must be 'world' or 'b-local', got {frame!r}")
     cfg = cfg or EngineConfig()
     rank, world = world_info(group)
     mine = list(frames_of_rank(len(transforms), rank, world))
+    local_b = frame == "b-local"
 
     def moved(f):
         xa, xb = transforms[f]
         return (mesh_a if xa is None else apply_transform(mesh_a, xa),
                 mesh_b if xb is None else apply_transform(mesh_b, xb))
 
+    def refit_frame(a, b):
+        if local_b:
+            refit(bvh_a, relative_mesh(a, b))
+        else:
+            refit(bvh_a, a)
+            refit(bvh_b, b)
+
     def row(r):
         w = r.witness
         return r.distance, (-1 if w is None else w.tri_a), (-1 if w is None else w.tri_b)
 
     local = {}
-    if not pipelined or not mine:
+    if not mine:
+        return gather_frames(len(transforms), local, group)
+    if local_b:
+        refit(bvh_b, mesh_b._root)  # B's boxes in its own frame, once
+    if not pipelined:
+        plan = None
         for f in mine:
             a, b = moved(f)
-            refit(bvh_a, a)
-            refit(bvh_b, b)
-            pq = _plan(a, b, bvh_a, bvh_b, cfg, kind, None)
-            local[f] = row(pq.run())
+            refit_frame(a, b)
+            if plan is None:
+                plan = PreparedQuery(a, b, bvh_a, bvh_b, cfg, kind, frame=frame)
+            local[f] = row(plan.bind(a, b).run())
         return gather_frames(len(transforms), local, group)
-    # two query plans with their own workspaces: frame i's query is launched
-    # before frame i-1's result is read, and frame i+1's refit (second stream)
-    # starts as soon as frame i's traversal has read the boxes
-    from .query import PreparedQuery
-
     qs = torch.cuda.current_stream()
     rs = torch.cuda.Stream()
     rs.wait_stream(qs)
@@ -135,8 +153,7 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
         with torch.cuda.stream(rs):
             if after is not None:
                 rs.wait_event(after)
-            refit(bvh_a, a)
-            refit(bvh_b, b)
+            refit_frame(a, b)
             done = torch.cuda.Event()
             done.record(rs)
         return done
@@ -144,7 +161,8 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
     cur = moved(mine[0])
     done = refit_on_rs(*cur)
     qs.wait_event(done)
-    plans = [PreparedQuery(cur[0], cur[1], bvh_a, bvh_b, cfg, kind, private_workspace=True) for _ in range(2)]
+    plans = [PreparedQuery(cur[0], cur[1], bvh_a, bvh_b, cfg, kind, private_workspace=True, frame=frame)
+             for _ in range(2)]
     pending = None
     for i, f in enumerate(mine):
         if i:

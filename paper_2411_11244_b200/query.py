@@ -288,13 +288,17 @@ class PreparedQuery:
     asynchronous; `collect()` does the single device->host copy."""
 
     def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, cfg: EngineConfig, kind: str, warm_pair=None,
-                 private_workspace: bool = False):
+                 private_workspace: bool = False, frame: str = "world"):
         _check_build(cfg, bvh_a, bvh_b)
+        if frame not in ("world", "b-local"):
+            raise ValueError(f"frame must be 'world' or 'b-local', got {frame!r}")
+        self.frame = frame
         self._pinned = self._ready = None
         self.kind = kind
         self.warm_pair = warm_pair
         self.trees = (bvh_a, bvh_b)
         self.g_cfg = _gd_config(cfg, kind, warm_pair)
+        self.g_cfg.frame = 1 if frame == "b-local" else 0
         self.bind(mesh_a, mesh_b)
         nbytes = C.c_size_t(0)
         L = _lib.lib()
@@ -311,8 +315,16 @@ class PreparedQuery:
             ta, tb = int(self.warm_pair[0]), int(self.warm_pair[1])
             if not (0 <= ta < mesh_a.n_triangles and 0 <= tb < mesh_b.n_triangles):
                 raise IndexError(f"warm_pair {self.warm_pair} out of range")
-        bvh_a.ensure_device(mesh_a)
-        bvh_b.ensure_device(mesh_b)
+        if self.frame == "b-local":
+            # boxes in B's local frame: B untransformed, A under the relative
+            # transform; the exact pass still sees the world meshes
+            from .mesh import relative_mesh
+
+            bvh_a.ensure_device(relative_mesh(mesh_a, mesh_b))
+            bvh_b.ensure_device(mesh_b._root)
+        else:
+            bvh_a.ensure_device(mesh_a)
+            bvh_b.ensure_device(mesh_b)
         self.meshes = (mesh_a, mesh_b)
         self.g_ma, self.g_mb = mesh_a.device_view(), mesh_b.device_view()
         self.g_a, self.g_b = bvh_a.device_view(), bvh_b.device_view()

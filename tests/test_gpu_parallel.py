@@ -124,9 +124,10 @@ def test_sequence_pipelining_and_inflight_queries(md, gpu):
     za, zb = md.build_f12(tz), md.build_f12(tbase)
     xfs = [md.ring_frame_transforms(f) for f in range(0, 90, 7)]
     for kind in ("min", "max"):
-        piped = md.run_sequence(tz, tbase, za, zb, xfs, kind)
+        piped = md.run_sequence(tz, tbase, za, zb, xfs, kind)  # world frame, pipelined
         plain = md.run_sequence(tz, tbase, za, zb, xfs, kind, pipelined=False)
-        assert np.array_equal(piped, plain), kind
+        local_b = md.run_sequence(tz, tbase, za, zb, xfs, kind, frame="b-local")
+        assert np.array_equal(piped, plain) and np.array_equal(piped, local_b), kind
     a, b = md.gen_scene("interlocked-rings", {"nu": 90, "nv": 45})
     ta, tb = md.build_f12(a), md.build_f12(b)
     cfg = md.EngineConfig()
