@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 8
+#define GDIST_ABI_VERSION 9
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -250,6 +250,16 @@ int gd_query_result_async(const GdConfig* cfg, void* workspace, void* host_dst, 
 int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* workspace,
                      const GdResult* result_dev, GdResult* out, GdIterStat* stats, int max_stats,
                      void* stream);
+
+/* Per-triangle DFS comparator (query.py:622-708 run_dfs_baseline): every
+ * triangle of A descends B's tree depth-first, nearer child first, pruning
+ * against one shared bound; synchronous.  `b` must be refit to mesh_b in the
+ * world frame (cfg->frame = 0); cfg->kind / precision / band_cap apply, the
+ * workspace is gd_query_workspace_size(b, b, cfg).  *visited_nodes = node
+ * examinations (pops), summed over A's triangles. */
+int gd_dfs_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* b, const GdConfig* cfg,
+                 void* workspace, size_t workspace_bytes, GdResult* out, int64_t* visited_nodes,
+                 void* stream);
 
 /* ---- OBJ ingest (mesh.py:112-163 load_obj), host only ------------------ */
 /* Parse a Wavefront OBJ file with the reference's semantics (v / f records,

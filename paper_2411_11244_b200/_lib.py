@@ -147,6 +147,8 @@ _SIGNATURES = {
     "gd_query_result_async": (C.c_int, [C.POINTER(GdConfig), P, P, C.c_int, P]),
     "gd_query_collect": (C.c_int, [C.POINTER(GdBvh), C.POINTER(GdBvh), C.POINTER(GdConfig), P, P,
                                    C.POINTER(GdResult), C.POINTER(GdIterStat), C.c_int, P]),
+    "gd_dfs_query": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdConfig), P,
+                               C.c_size_t, C.POINTER(GdResult), C.POINTER(C.c_int64), P]),
     "gd_obj_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                               C.POINTER(C.c_int64)]),
     "gd_obj_read": (C.c_int, [P, P, P]),

@@ -31,6 +31,8 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
 void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, GdResult* out, GdIterStat* stats,
                    int max_stats, cudaStream_t s);
+void dfs_query(const GdMesh& ma, const GdMesh& mb, const GdBvh& b, const GdConfig& cfg, void* ws, size_t ws_bytes,
+               GdResult* out, int64_t* visited, cudaStream_t s);
 void tri_tri_batch(int kind, int precision, const void* t1, const void* t2, int64_t n, void* d, void* p, void* q,
                    cudaStream_t s);
 void tri_tri_fast(int kind, const float* t1, const float* t2, int64_t n, float* d, cudaStream_t s);
@@ -220,6 +222,16 @@ int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* 
     (void)a;
     (void)b;
     query_collect(*cfg, workspace, result_dev, out, stats, max_stats, S(stream));
+  });
+}
+
+int gd_dfs_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* b, const GdConfig* cfg, void* workspace,
+                 size_t workspace_bytes, GdResult* out, int64_t* visited_nodes, void* stream) {
+  return guarded([&] {
+    GD_CHECK(mesh_a && mesh_b && b && cfg && out, GD_ERR_INVALID, "null argument");
+    dfs_query(*mesh_a, *mesh_b, *b, *cfg, workspace, workspace_bytes, out, visited_nodes, S(stream));
+    if (out->status == GD_ERR_WORKSPACE)
+      throw Failure{GD_ERR_WORKSPACE, "DFS band overflow: raise GdConfig.band_cap"};
   });
 }
 

@@ -63,6 +63,8 @@ struct alignas(16) QState {
   int band_overflow;
   unsigned bar;                      // grid-barrier arrivals (k_traverse)
   unsigned fbest;                    // best float32 narrow distance (ordered bits)
+  unsigned dfs_coord;                // per-triangle DFS: max |coordinate| of A (float bits)
+  unsigned long long visited;        // per-triangle DFS: node examinations
   unsigned long long cnt[kMaxIters + 1];       // iteration i: survivors (low 40 bits) + arrivals
   unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
   unsigned long long skip_it[kMaxIters];       // candidates of pairs another split rank owns

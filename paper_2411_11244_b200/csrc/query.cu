@@ -21,7 +21,7 @@
 #include <cstddef>
 #include <cstring>
 
-#include "narrow.cuh"
+#include "dfs.cuh"
 
 namespace gd {
 
@@ -149,9 +149,8 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
   count_launches(kMax ? 5 : 6);
 }
 
-void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
-                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done) {
-  validate(a, b, cfg);
+static QArgs make_args(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
+                       void* ws, size_t ws_bytes, GdResult* result_dev) {
   WsLayout L = ws_layout(cfg);
   GD_CHECK(ws != nullptr && ws_bytes >= L.total, GD_ERR_WORKSPACE,
            "query workspace too small: need " + std::to_string(L.total) + " bytes");
@@ -182,6 +181,13 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
   q.cap = L.cap;
   q.band_cap = L.band_cap;
   q.result = result_dev;  // nullptr: the record stays in the state block (QState::res)
+  return q;
+}
+
+void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
+                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done) {
+  validate(a, b, cfg);
+  QArgs q = make_args(ma, mb, a, b, cfg, ws, ws_bytes, result_dev);
   if (g_profile) g_last_state = q.S;
   if (cfg.kind == 1)
     launch_query<true>(q, s, traversal_done);
@@ -217,6 +223,47 @@ void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, Gd
   GD_CUDA(cudaStreamSynchronize(s));
   memcpy(out, g_pinned, sizeof(GdResult));
   if (ns) memcpy(stats, g_pinned + sizeof(GdResult), sizeof(GdIterStat) * ns);
+}
+
+}  // namespace gd
+
+namespace gd {
+
+// per-triangle DFS comparator (dfs.cuh): scale, state, descent, exact pass
+__global__ void k_dfs_check(QState* S) {
+  if (S->band_overflow) S->err = GD_ERR_WORKSPACE;  // no rescan path here
+}
+
+template <bool kMax>
+static void launch_dfs(const QArgs& q, cudaStream_t s) {
+  const int sms = num_sms();
+  GD_CUDA(cudaMemsetAsync(&q.S->dfs_coord, 0, sizeof(unsigned), s));
+  k_dfs_scale<<<sms * 2, 256, 0, s>>>(q.ma, q.S);
+  k_dfs_init<kMax><<<1, 1, 0, s>>>(q);
+  const long long m = q.ma.m;
+  if (m > 0) k_dfs<kMax><<<(unsigned)((m + kDfsThreads - 1) / kDfsThreads), kDfsThreads, 0, s>>>(q);
+  k_dfs_check<<<1, 1, 0, s>>>(q.S);
+  k_bandsel<kMax><<<sms, 256, 0, s>>>(q);
+  k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);
+  GD_CUDA(cudaGetLastError());
+  count_launches(m > 0 ? 6 : 5);
+}
+
+void dfs_query(const GdMesh& ma, const GdMesh& mb, const GdBvh& b, const GdConfig& cfg, void* ws, size_t ws_bytes,
+               GdResult* out, int64_t* visited, cudaStream_t s) {
+  validate(b, b, cfg);
+  GD_CHECK(cfg.frame == 0, GD_ERR_CONFIG, "the DFS comparator traverses in the world frame (frame = 0)");
+  GD_CHECK(ma.m < (1ll << 32), GD_ERR_INVALID, "mesh A too large");
+  QArgs q = make_args(ma, mb, b, b, cfg, ws, ws_bytes, nullptr);
+  if (cfg.kind == 1)
+    launch_dfs<true>(q, s);
+  else
+    launch_dfs<false>(q, s);
+  query_collect(cfg, ws, nullptr, out, nullptr, 0, s);
+  unsigned long long v = 0;
+  GD_CUDA(cudaMemcpyAsync(&v, &q.S->visited, sizeof v, cudaMemcpyDeviceToHost, s));
+  GD_CUDA(cudaStreamSynchronize(s));
+  if (visited) *visited = (int64_t)v;
 }
 
 }  // namespace gd

@@ -568,8 +568,27 @@ def expand_front(front: Front, k: int, state: QueryState, bvh_a: F12Bvh, bvh_b: 
 
 
 def run_dfs_baseline(mesh_a, mesh_b, bvh_b, kind: str = "min") -> QueryResult:
-    """Per-triangle DFS comparator (query.py:622-708) -- the paper's naive
-    GPU baseline; see dfs.py."""
-    from .dfs import run_dfs
-
-    return run_dfs(mesh_a, mesh_b, bvh_b, kind)
+    """Per-triangle descent comparator (query.py:622-708): every triangle of
+    A walks B's tree depth-first, nearer child first, pruning against one
+    shared monotone bound (csrc/dfs.cuh, one device thread per triangle).
+    Same distance as the front engine (float64 exact pass); `visited_nodes`
+    counts node examinations.  No iterations, expanded_pairs = 0."""
+    if kind not in ("min", "max"):
+        raise ValueError(f"kind must be 'min' or 'max', got {kind!r}")
+    if mesh_a.n_triangles == 0:
+        return QueryResult(kind, float("inf") if kind == "min" else float("-inf"), None, (), 0, 0, visited_nodes=0)
+    g = _gd_config(EngineConfig(), kind, None)
+    g.precision = 64  # the reference walks float64 triangle points
+    bvh_b.ensure_device(mesh_b)
+    g_ma, g_mb, g_b = mesh_a.device_view(), mesh_b.device_view(), bvh_b.device_view()
+    L = _lib.lib()
+    nbytes = C.c_size_t(0)
+    _lib.check(L.gd_query_workspace_size(C.byref(g_b), C.byref(g_b), C.byref(g), C.byref(nbytes)),
+               "query_workspace_size")
+    ws = _Workspace.get(nbytes.value)
+    r, visited = _lib.GdResult(), C.c_int64(0)
+    _lib.check(L.gd_dfs_query(C.byref(g_ma), C.byref(g_mb), C.byref(g_b), C.byref(g), _lib.ptr(ws), ws.numel(),
+                              C.byref(r), C.byref(visited), _lib.stream_ptr()), "dfs_query")
+    res = _result(kind, r, ())
+    return QueryResult(kind, res.distance, res.witness, (), 0, res.narrow_pairs, visited_nodes=int(visited.value),
+                       band_pairs=res.band_pairs)

@@ -274,3 +274,33 @@ def test_expand_front_step_api(md, gpu, oracle):
     assert st.bound == want.distance
     assert [(s.k, s.front_in, s.front_out, s.culled, s.bound_after) for s in st.iterations] == [
         tuple(x) for x in want.iterations]
+
+
+def test_dfs_comparator(md, gpu, golden_meta, oracle):
+    """run_dfs_baseline (query.py:622-708): the per-triangle descent returns
+    the reference's exact float64 distance and the brute-force witness, and
+    counts its node examinations."""
+    for rec in golden_meta["engine"][:12]:
+        ma, mb = md.gen_scene(rec["kind"], rec["params"])
+        tb = md.build_f12(mb)
+        for q in ("min", "max"):
+            g = rec[f"{q}64"]
+            r = md.run_dfs_baseline(ma, mb, tb, q)
+            assert r.distance == g["brute_distance"], (rec["kind"], q)
+            assert (r.witness.tri_a, r.witness.tri_b) == (g["brute_tri_a"], g["brute_tri_b"])
+            assert r.witness_exact and r.iterations == () and r.expanded_pairs == 0
+            assert r.visited_nodes >= ma.n_triangles and r.narrow_pairs > 0
+    # depth-0 trees, moved meshes, float32-built trees
+    a1 = md.TriangleMesh([[0, 0, 0.0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]])
+    big, _ = md.gen_scene("interlocked-rings", {"nu": 60, "nv": 40})
+    ring, other = md.gen_scene("interlocked-rings", {"nu": 30, "nv": 20})
+    xf = md.RigidTransform.from_axis_angle((0.2, 1, 0.3), 0.7, (0.3, -0.1, 0.2))
+    for ma, mb, dt in ((a1, a1, np.float64), (a1, big, np.float64), (big, a1, np.float64),
+                       (md.apply_transform(ring, xf), other, np.float32)):
+        tb = md.build_f12(mb, dtype=dt)
+        for q in ("min", "max"):
+            r = md.run_dfs_baseline(ma, mb, tb, q)
+            d, ia, ib, _, _ = oracle.brute_force(ma.triangle_points(), mb.triangle_points(), q, force=True)
+            assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (ia, ib), (q, ma.n_triangles)
+    with pytest.raises(ValueError):
+        md.run_dfs_baseline(a1, a1, md.build_f12(a1), "mean")
