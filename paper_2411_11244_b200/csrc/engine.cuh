@@ -181,16 +181,19 @@ __device__ __forceinline__ Box tri_box(const Tri<float>& t) {
   return b;
 }
 
-// float64 vertex of a mesh with its rigid transform applied (mesh.py:102-105)
+// float64 vertex of a mesh with its rigid transform applied (mesh.py:102-105:
+// `V @ R.T + t`).  numpy's matmul is OpenBLAS dgemm, whose kernels accumulate
+// over k with fused multiply-adds, x' = fma(R02, z, fma(R01, y, R00 x)), and
+// the translation is a separate add -- reproduced here, so a moved mesh has
+// the reference's vertex bits (tests/test_gpu_parity.py).
 __device__ __forceinline__ V3<double> mesh_vertex(const GdMesh& m, long long i) {
   const double* p = m.vtx + 3 * i;
   double x = p[0], y = p[1], z = p[2];
   if (!m.has_xf) return {x, y, z};
   const double* R = m.rot;
-  using E = Exact<double>;
-  return {E::add(E::add(E::add(E::mul(R[0], x), E::mul(R[1], y)), E::mul(R[2], z)), m.trans[0]),
-          E::add(E::add(E::add(E::mul(R[3], x), E::mul(R[4], y)), E::mul(R[5], z)), m.trans[1]),
-          E::add(E::add(E::add(E::mul(R[6], x), E::mul(R[7], y)), E::mul(R[8], z)), m.trans[2])};
+  return {__dadd_rn(__fma_rn(R[2], z, __fma_rn(R[1], y, __dmul_rn(R[0], x))), m.trans[0]),
+          __dadd_rn(__fma_rn(R[5], z, __fma_rn(R[4], y, __dmul_rn(R[3], x))), m.trans[1]),
+          __dadd_rn(__fma_rn(R[8], z, __fma_rn(R[7], y, __dmul_rn(R[6], x))), m.trans[2])};
 }
 
 template <typename T>

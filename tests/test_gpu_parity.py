@@ -124,10 +124,9 @@ def test_refit_moved_mesh(md, gpu, oracle):
     # same topology, boxes recomputed from the reference's moved vertices
     ref = oracle.Tree(np.empty((t.n_nodes, 3)), np.empty((t.n_nodes, 3)), t.leaf_tris, t.prim_order, t.depth)
     oracle.fill_boxes(ref, moved.vertices, moved.triangles)
-    # device transform vs numpy dgemm differ by <= 1 ulp per coordinate
-    assert np.allclose(t.node_min, ref.node_min, rtol=0, atol=4e-15 * np.abs(ref.node_min).max())
-    assert np.allclose(t.node_max, ref.node_max, rtol=0, atol=4e-15 * np.abs(ref.node_max).max())
-    # a refit with an explicitly materialised mesh is bitwise the reference
+    # the lazy device transform reproduces numpy's dgemm vertices bit for bit
+    assert np.array_equal(t.node_min, ref.node_min) and np.array_equal(t.node_max, ref.node_max)
+    # so does a refit with an explicitly materialised mesh
     md.refit(t, md.TriangleMesh(moved.vertices, moved.triangles))
     assert np.array_equal(t.node_min, ref.node_min) and np.array_equal(t.node_max, ref.node_max)
     with pytest.raises(md.TopologyMismatchError):
@@ -135,7 +134,7 @@ def test_refit_moved_mesh(md, gpu, oracle):
     # translation commutes with min/max (SPEC refit example)
     t2 = md.build_f12(a)
     md.refit(t2, md.apply_transform(a, md.RigidTransform(np.eye(3), (1.0, 2.0, 3.0))))
-    assert np.allclose(t2.node_min, md.build_f12(a).node_min + [1.0, 2.0, 3.0], atol=1e-12)
+    assert np.array_equal(t2.node_min, md.build_f12(a).node_min + [1.0, 2.0, 3.0])
 
 
 def _check_query(md, ma, mb, prec, rec_q, tag):
@@ -177,9 +176,9 @@ def test_config1_tori_golden(md, gpu, golden_meta):
 
 
 def test_rotation_frames_golden(md, gpu, golden_meta):
-    """Config-3 frames through the lazy device transform + refit: distances
-    within 1e-12 relative of the reference (its vertices come from numpy's
-    dgemm, ours from the device formula), identical witnesses."""
+    """Config-3 frames through the lazy device transform + refit: the
+    reference's distances and witnesses bit for bit (the device transform
+    follows numpy's dgemm arithmetic, engine.cuh mesh_vertex)."""
     tz, tb = md.ring_pair_base(100, 50)
     bvh_a, bvh_b = md.build_f12(tz), md.build_f12(tb)
     for rec in golden_meta["frames"]:
@@ -189,10 +188,10 @@ def test_rotation_frames_golden(md, gpu, golden_meta):
         md.refit(bvh_b, b)
         for q in ("min", "max"):
             r = (md.run_min_query if q == "min" else md.run_max_query)(a, b, bvh_a, bvh_b)
-            assert abs(r.distance - rec[q]["distance"]) <= 1e-12 * rec[q]["distance"], (rec["frame"], q)
+            assert r.distance == rec[q]["distance"], (rec["frame"], q)
             assert (r.witness.tri_a, r.witness.tri_b) == (rec[q]["tri_a"], rec[q]["tri_b"])
         d, pair = md.min_distance(tz, b, xa)
-        assert abs(d - rec["min"]["distance"]) <= 1e-12 * d and pair == (rec["min"]["tri_a"], rec["min"]["tri_b"])
+        assert d == rec["min"]["distance"] and pair == (rec["min"]["tri_a"], rec["min"]["tri_b"])
 
 
 def test_brute_force_device(md, gpu, golden_meta):
