@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 9
+#define GDIST_ABI_VERSION 10
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -133,6 +133,12 @@ typedef struct GdConfig {
    * tree per frame.  The exact pass always works in world coordinates, so
    * the answer is bitwise the world-frame one. */
   int32_t frame;
+  /* temporal warm start: a DEVICE GdResult -- e.g.
+   * the previous frame's record, gd_query_result_device -- read when the
+   * query starts; if its status is 0 and tri_a >= 0, that pair seeds the
+   * bound exactly as warm_a / warm_b do.  NULL = none.  Stream order makes
+   * it safe: the producing query ran earlier on the same stream. */
+  const void* warm_from;
 } GdConfig;
 
 /* QueryResult (query.py:230-263) + Witness (query.py:136-144). */
@@ -246,6 +252,9 @@ int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a
  * sizeof(GdResult) + max_stats * sizeof(GdIterStat) bytes) on `stream`;
  * the caller synchronises (e.g. an event).  Lets several queries, each with
  * its own workspace, be in flight. */
+/* Device address of the result record inside a query workspace (valid
+ * after a query on that workspace completes in stream order). */
+int gd_query_result_device(const GdConfig* cfg, void* workspace, const void** out);
 int gd_query_result_async(const GdConfig* cfg, void* workspace, void* host_dst, int max_stats, void* stream);
 int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* workspace,
                      const GdResult* result_dev, GdResult* out, GdIterStat* stats, int max_stats,

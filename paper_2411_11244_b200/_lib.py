@@ -85,6 +85,7 @@ class GdConfig(C.Structure):
         ("split_world", C.c_int32),
         ("split_level", C.c_int32),
         ("frame", C.c_int32),
+        ("warm_from", C.c_void_p),
     ]
 
 
@@ -144,6 +145,7 @@ _SIGNATURES = {
                                  C.POINTER(GdConfig), P, C.c_size_t, P, P]),
     "gd_query_async_ev": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
                                     C.POINTER(GdConfig), P, C.c_size_t, P, P, P]),
+    "gd_query_result_device": (C.c_int, [C.POINTER(GdConfig), P, C.POINTER(C.c_void_p)]),
     "gd_query_result_async": (C.c_int, [C.POINTER(GdConfig), P, P, C.c_int, P]),
     "gd_query_collect": (C.c_int, [C.POINTER(GdBvh), C.POINTER(GdBvh), C.POINTER(GdConfig), P, P,
                                    C.POINTER(GdResult), C.POINTER(GdIterStat), C.c_int, P]),

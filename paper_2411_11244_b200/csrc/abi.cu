@@ -28,6 +28,7 @@ void pair_greedy(const double* sa, int64_t n, uint8_t* is_left);
 size_t query_workspace_size(const GdConfig& cfg);
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done);
+const void* query_result_device(const GdConfig& cfg, void* ws);
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
 void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, GdResult* out, GdIterStat* stats,
                    int max_stats, cudaStream_t s);
@@ -212,6 +213,13 @@ int gd_query_result_async(const GdConfig* cfg, void* workspace, void* host_dst, 
   return guarded([&] {
     GD_CHECK(cfg && workspace && host_dst, GD_ERR_INVALID, "null argument");
     query_result_async(*cfg, workspace, host_dst, max_stats, S(stream));
+  });
+}
+
+int gd_query_result_device(const GdConfig* cfg, void* workspace, const void** out) {
+  return guarded([&] {
+    GD_CHECK(cfg && workspace && out, GD_ERR_INVALID, "null argument");
+    *out = query_result_device(*cfg, workspace);
   });
 }
 

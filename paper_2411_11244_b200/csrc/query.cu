@@ -200,6 +200,11 @@ static_assert(offsetof(QState, stats) == offsetof(QState, res) + sizeof(GdResult
 
 // enqueue the result record + stats copy into caller-provided (pinned) host
 // memory; the caller synchronises (event) -- lets several queries be in flight
+const void* query_result_device(const GdConfig& cfg, void* ws) {
+  WsLayout L = ws_layout(cfg);
+  return &reinterpret_cast<const QState*>(static_cast<char*>(ws) + L.state)->res;
+}
+
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s) {
   WsLayout L = ws_layout(cfg);
   const QState* S = reinterpret_cast<const QState*>(static_cast<char*>(ws) + L.state);

@@ -168,9 +168,17 @@ __device__ void init_query(const QArgs& q) {
   } else {
     S->n_in = 1;
   }
-  if (q.cfg.warm_a >= 0) {
+  long long wa = q.cfg.warm_a, wb = q.cfg.warm_b;
+  if (q.cfg.warm_from) {  // the previous frame's witness (GdConfig.warm_from)
+    const GdResult* w = static_cast<const GdResult*>(q.cfg.warm_from);
+    if (w->status == 0 && w->tri_a >= 0 && w->tri_a < q.ma.m && w->tri_b >= 0 && w->tri_b < q.mb.m) {
+      wa = w->tri_a;
+      wb = w->tri_b;
+    }
+  }
+  if (wa >= 0) {
     // warm_pair seeds the bound with one exact pair (query.py:494-502)
-    unsigned ta = (unsigned)q.cfg.warm_a, tb = (unsigned)q.cfg.warm_b;
+    unsigned ta = (unsigned)wa, tb = (unsigned)wb;
     const int32_t* ia = q.ma.tri + 3 * (long long)ta;
     const int32_t* ib = q.mb.tri + 3 * (long long)tb;
     // the pair always reaches the exact pass (band distance -inf / +inf);

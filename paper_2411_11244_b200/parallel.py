@@ -84,7 +84,7 @@ def run_frames(n_frames: int, frame_fn, group=None, device=None) -> np.ndarray:
 
 
 def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cfg=None, group=None,
-                 pipelined: bool = True, frame: str = "world") -> np.ndarray:
+                 pipelined: bool = True, frame: str = "world", warm: bool = False) -> np.ndarray:
     """Distance over a rigid-motion sequence, frames sharded over the ranks.
 
     transforms: list of (xf_a, xf_b) RigidTransform pairs (either may be
@@ -101,7 +101,9 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
     pipelined: the refit for frame f+1 runs on a second stream as soon as
     frame f's traversal has read the boxes (gd_query_async_ev), overlapping
     frame f's narrow and exact phases, and two query plans are in flight so
-    the host never waits on the GPU between frames."""
+    the host never waits on the GPU between frames.
+    warm: seed each frame's bound with the previous frame's witness pair on
+    the device (PreparedQuery.seed_from; temporal coherence, exact)."""
     import torch
 
     from .bvh import refit
@@ -142,7 +144,9 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
             a, b = moved(f)
             refit_frame(a, b)
             if plan is None:
-                plan = PreparedQuery(a, b, bvh_a, bvh_b, cfg, kind, frame=frame)
+                plan = PreparedQuery(a, b, bvh_a, bvh_b, cfg, kind, private_workspace=warm, frame=frame)
+            elif warm:
+                plan.seed_from(plan)
             local[f] = row(plan.bind(a, b).run())
         return gather_frames(len(transforms), local, group)
     qs = torch.cuda.current_stream()
@@ -168,6 +172,8 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
         if i:
             qs.wait_event(done)
         pq = plans[i % 2].bind(*cur)
+        if warm and i:
+            pq.seed_from(plans[(i - 1) % 2])
         trav = torch.cuda.Event()
         pq.launch_fetch(traversal_done=trav)
         if i + 1 < len(mine):

@@ -354,6 +354,22 @@ class PreparedQuery:
         self.launch()
         return self.collect()
 
+    def seed_from(self, other: "PreparedQuery | None"):
+        """Temporal warm start: seed this query's
+        bound with `other`'s witness pair, read on the device when this query
+        starts (GdConfig.warm_from), so no host round trip is needed between
+        frames.  `other` must have been launched earlier on the same stream
+        (it may be this query: the record is read before it is rewritten).
+        Exact like warm_pair: only the work changes."""
+        if other is None:
+            self.g_cfg.warm_from = None
+            return self
+        p = C.c_void_p()
+        _lib.check(_lib.lib().gd_query_result_device(C.byref(other.g_cfg), _lib.ptr(other.ws), C.byref(p)),
+                   "query_result_device")
+        self.g_cfg.warm_from = p.value
+        return self
+
     # -- several queries in flight (each PreparedQuery with its own workspace)
     def launch_fetch(self, stream=None, traversal_done=None):
         """launch() + an asynchronous copy of the result record and stats to

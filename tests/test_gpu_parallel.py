@@ -128,6 +128,10 @@ def test_sequence_pipelining_and_inflight_queries(md, gpu):
         plain = md.run_sequence(tz, tbase, za, zb, xfs, kind, pipelined=False)
         local_b = md.run_sequence(tz, tbase, za, zb, xfs, kind, frame="b-local")
         assert np.array_equal(piped, plain) and np.array_equal(piped, local_b), kind
+        # temporal warm start (device-side seed from the previous frame's record)
+        warm = md.run_sequence(tz, tbase, za, zb, xfs, kind, warm=True)
+        warm_plain = md.run_sequence(tz, tbase, za, zb, xfs, kind, pipelined=False, warm=True)
+        assert np.array_equal(piped, warm) and np.array_equal(piped, warm_plain), kind
     a, b = md.gen_scene("interlocked-rings", {"nu": 90, "nv": 45})
     ta, tb = md.build_f12(a), md.build_f12(b)
     cfg = md.EngineConfig()
@@ -141,3 +145,28 @@ def test_sequence_pipelining_and_inflight_queries(md, gpu):
         assert r.distance == want.distance and (r.witness.tri_a, r.witness.tri_b) == (want.witness.tri_a,
                                                                                        want.witness.tri_b)
         assert len(r.iterations) == len(want.iterations)  # front sizes depend on bound timing; depths do not
+
+
+def test_seed_from_previous_frame(md, gpu):
+    """PreparedQuery.seed_from: the seeded query returns the cold answer with
+    no more expanded pairs than the cold run, also when the source record
+    belongs to another scene's query (any pair is a valid seed)."""
+    from paper_2411_11244_b200 import query as Q
+
+    tz, tbase = md.ring_pair_base(120, 60)
+    za, zb = md.build_f12(tz), md.build_f12(tbase)
+    cfg = md.EngineConfig()
+    xa, xb = md.ring_frame_transforms(10)
+    a0, b0 = md.apply_transform(tz, xa), md.apply_transform(tbase, xb)
+    for kind in ("min", "max"):
+        src = Q.PreparedQuery(a0, b0, za, zb, cfg, kind, private_workspace=True)
+        src.run()
+        xa, xb = md.ring_frame_transforms(11)
+        a1, b1 = md.apply_transform(tz, xa), md.apply_transform(tbase, xb)
+        cold = (md.run_min_query if kind == "min" else md.run_max_query)(a1, b1, za, zb, cfg)
+        pq = Q.PreparedQuery(a1, b1, za, zb, cfg, kind, private_workspace=True).seed_from(src)
+        r = pq.run()
+        assert r.distance == cold.distance and (r.witness.tri_a, r.witness.tri_b) == (cold.witness.tri_a,
+                                                                                      cold.witness.tri_b)
+        assert r.expanded_pairs <= cold.expanded_pairs
+        assert pq.seed_from(None).g_cfg.warm_from is None
