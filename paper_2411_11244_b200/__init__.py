@@ -10,55 +10,30 @@ intended switch.  Extra entry points named by BASELINE.json:
 
 from __future__ import annotations
 
+import importlib
 import weakref
 
-from .bounds import (
-    aabb_max_upper,
-    aabb_min_lower,
-    batch_enhanced_max_lower,
-    batch_enhanced_min_upper,
-    batch_max_upper,
-    batch_min_lower,
-    batch_tri_tri_max,
-    batch_tri_tri_min,
-    enhanced_max_lower,
-    enhanced_min_upper,
-    tri_tri_max,
-    tri_tri_min,
-)
-from .bvh import Aabb, F12Bvh, build_f12, descendant, morton_codes, node_level, refit, remaining_depth
-from .errors import (
-    ConfigError,
-    DegenerateTriangleError,
-    FrontOverflowError,
-    MeshDistError,
-    ObjParseError,
-    SceneError,
-    SizeGuardError,
-    TightnessError,
-    TopologyMismatchError,
-)
-from .mesh import RigidTransform, TriangleMesh, apply_transform, load_obj, relative_mesh
-from .query import (
-    EngineConfig,
-    Front,
-    FrontEntry,
-    IterationStat,
-    PreparedQuery,
-    QueryResult,
-    QueryState,
-    Witness,
-    adaptive_depth,
-    brute_force_max,
-    brute_force_min,
-    expand_front,
-    process_leaf_pair,
-    run_dfs_baseline,
-    run_max_query,
-    run_min_query,
-)
-from .parallel import run_sequence, run_split_query
-from .scenes import gen_scene, ring_frame_transforms, ring_pair_base, scene_kinds, torus_mesh
+# public names by defining module (reference __init__.py:8-95 plus the
+# multi-GPU / sequence / comparator entry points of this package)
+_EXPORTS = {
+    "bounds": "aabb_max_upper aabb_min_lower batch_enhanced_max_lower batch_enhanced_min_upper batch_max_upper "
+              "batch_min_lower batch_tri_tri_max batch_tri_tri_min enhanced_max_lower enhanced_min_upper "
+              "tri_tri_max tri_tri_min",
+    "bvh": "Aabb F12Bvh build_f12 descendant morton_codes node_level refit remaining_depth",
+    "errors": "ConfigError DegenerateTriangleError FrontOverflowError MeshDistError ObjParseError SceneError "
+              "SizeGuardError TightnessError TopologyMismatchError",
+    "mesh": "RigidTransform TriangleMesh apply_transform load_obj relative_mesh",
+    "query": "EngineConfig Front FrontEntry IterationStat PreparedQuery QueryResult QueryState Witness "
+             "adaptive_depth brute_force_max brute_force_min expand_front process_leaf_pair run_dfs_baseline "
+             "run_max_query run_min_query",
+    "parallel": "run_sequence run_split_query",
+    "scenes": "gen_scene ring_frame_transforms ring_pair_base scene_kinds torus_mesh",
+}
+for _module, _names in _EXPORTS.items():
+    _m = importlib.import_module("." + _module, __name__)
+    for _name in _names.split():
+        globals()[_name] = getattr(_m, _name)
+del _module, _names, _m, _name
 
 __version__ = "0.1.0"
 
@@ -104,65 +79,5 @@ def max_distance(mesh_a: TriangleMesh, mesh_b: TriangleMesh, transform: RigidTra
     return _distance("max", mesh_a, mesh_b, transform, cfg)
 
 
-__all__ = [
-    "Aabb",
-    "ConfigError",
-    "DegenerateTriangleError",
-    "EngineConfig",
-    "F12Bvh",
-    "Front",
-    "FrontEntry",
-    "FrontOverflowError",
-    "IterationStat",
-    "MeshDistError",
-    "ObjParseError",
-    "PreparedQuery",
-    "QueryResult",
-    "QueryState",
-    "RigidTransform",
-    "SceneError",
-    "SizeGuardError",
-    "TightnessError",
-    "TopologyMismatchError",
-    "TriangleMesh",
-    "Witness",
-    "aabb_max_upper",
-    "aabb_min_lower",
-    "adaptive_depth",
-    "apply_transform",
-    "batch_enhanced_max_lower",
-    "batch_enhanced_min_upper",
-    "batch_max_upper",
-    "batch_min_lower",
-    "batch_tri_tri_max",
-    "batch_tri_tri_min",
-    "brute_force_max",
-    "brute_force_min",
-    "build_f12",
-    "descendant",
-    "enhanced_max_lower",
-    "enhanced_min_upper",
-    "expand_front",
-    "gen_scene",
-    "load_obj",
-    "max_distance",
-    "min_distance",
-    "morton_codes",
-    "node_level",
-    "process_leaf_pair",
-    "refit",
-    "relative_mesh",
-    "remaining_depth",
-    "ring_frame_transforms",
-    "ring_pair_base",
-    "run_dfs_baseline",
-    "run_max_query",
-    "run_min_query",
-    "run_sequence",
-    "run_split_query",
-    "scene_kinds",
-    "torus_mesh",
-    "tri_tri_max",
-    "tri_tri_min",
-    "__version__",
-]
+__all__ = sorted([n for names in _EXPORTS.values() for n in names.split()] + ["max_distance", "min_distance"]) + [
+    "__version__"]
