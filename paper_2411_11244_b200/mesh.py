@@ -76,10 +76,52 @@ class TriangleMesh:
         out._gview = None
         return out
 
+    def deformed(self, vertices) -> "TriangleMesh":
+        """Same connectivity, new base vertex positions (deformable meshes,
+        SURVEY.md 8(f) row 2): `refit(bvh, mesh.deformed(V))` keeps the tree's
+        topology and re-stages the vertices on the device.  `vertices` is an
+        (n_vertices, 3) array, or a float64 CUDA tensor of that shape used in
+        place -- a simulation that keeps its vertices on the GPU never sends
+        them through the host (`.vertices` downloads them only if read).
+        Transforms applied to `self` are not carried over."""
+        root = self._root
+        out = TriangleMesh.__new__(TriangleMesh)
+        out._triangles = root._triangles
+        out._root = out
+        out._chain = ()
+        out._rot = out._trans = None
+        out._gview = None
+        torch = _lib.torch()
+        if isinstance(vertices, torch.Tensor) and vertices.is_cuda:
+            if tuple(vertices.shape) != (root.n_vertices, 3) or vertices.dtype != torch.float64:
+                raise ValueError(f"deformed vertices must be a ({root.n_vertices}, 3) float64 tensor, "
+                                 f"got {tuple(vertices.shape)} {vertices.dtype}")
+            out._vertices = None
+            out._dev = (vertices.contiguous(), root._upload()[1])
+            return out
+        v = np.array(vertices, dtype=np.float64, order="C")
+        if v.shape != (root.n_vertices, 3):
+            raise ValueError(f"deformed vertices must be ({root.n_vertices}, 3), got {v.shape}")
+        v.setflags(write=False)
+        out._vertices = v
+        out._dev = None
+        if root._dev is not None:  # share the uploaded connectivity, send only the vertices
+            out._dev = (torch.from_numpy(v.copy()).to(root._dev[1].device), root._dev[1])
+        return out
+
+    def _host_vertices(self) -> np.ndarray:
+        """Base vertices on the host (downloaded once for a device-made mesh)."""
+        root = self._root
+        if root._vertices is None:
+            v = root._dev[0].cpu().numpy()
+            v.setflags(write=False)
+            root._vertices = v
+        return root._vertices
+
     @property
     def vertices(self) -> np.ndarray:
         if self._vertices is None:
-            v = self._root._vertices
+            v = self._host_vertices()
             for xf in self._chain:
                 v = v @ xf.rotation.T + xf.translation  # mesh.py:104, transform by transform
             v = np.ascontiguousarray(v)
@@ -97,7 +139,8 @@ class TriangleMesh:
 
     @property
     def n_vertices(self) -> int:
-        return len(self._root._vertices)
+        root = self._root
+        return len(root._vertices) if root._vertices is not None else int(root._dev[0].shape[0])
 
     def triangle_points(self, dtype=np.float64) -> np.ndarray:
         """(m, 3, 3) corners: cast first, then gather (mesh.py:64-66)."""

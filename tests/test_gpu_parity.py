@@ -303,3 +303,38 @@ def test_dfs_comparator(md, gpu, golden_meta, oracle):
             assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (ia, ib), (q, ma.n_triangles)
     with pytest.raises(ValueError):
         md.run_dfs_baseline(a1, a1, md.build_f12(a1), "mean")
+
+
+def test_deformed_meshes(md, gpu, oracle):
+    """Deformable refit: TriangleMesh.deformed with host
+    arrays or a float64 CUDA tensor (used in place) refits the same tree and
+    answers exactly like a mesh built from the same vertices."""
+    import torch
+
+    a, b = md.gen_scene("interlocked-rings", {"nu": 30, "nv": 20})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    md.run_min_query(a, b, ta, tb)
+    rng = np.random.default_rng(3)
+    for step in range(3):
+        V = a.vertices + 0.01 * rng.normal(size=a.vertices.shape)
+        for src in (V, torch.tensor(V, device="cuda")):
+            d = a.deformed(src)
+            assert d.n_vertices == a.n_vertices and d.triangles is a.triangles
+            md.refit(ta, d)
+            fresh = md.TriangleMesh(V, a.triangles)
+            for q in ("min", "max"):
+                r = (md.run_min_query if q == "min" else md.run_max_query)(d, b, ta, tb)
+                dd, ia, ib, _, _ = oracle.brute_force(fresh.triangle_points(), b.triangle_points(), q, force=True)
+                assert r.distance == dd and (r.witness.tri_a, r.witness.tri_b) == (ia, ib), (step, q)
+            assert np.array_equal(d.vertices, V)
+    # transformed deformed mesh, boxes equal the reference's on the moved vertices
+    xf = md.RigidTransform.from_axis_angle((0, 1, 1), 0.4, (0.1, 0.2, 0.3))
+    moved = md.apply_transform(a.deformed(torch.tensor(V, device="cuda")), xf)
+    md.refit(ta, moved)
+    ref = oracle.Tree(np.empty((ta.n_nodes, 3)), np.empty((ta.n_nodes, 3)), ta.leaf_tris, ta.prim_order, ta.depth)
+    oracle.fill_boxes(ref, moved.vertices, moved.triangles)
+    assert np.array_equal(ta.node_min, ref.node_min) and np.array_equal(ta.node_max, ref.node_max)
+    with pytest.raises(ValueError):
+        a.deformed(torch.zeros((3, 3), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError):
+        a.deformed(np.zeros((a.n_vertices + 1, 3)))
