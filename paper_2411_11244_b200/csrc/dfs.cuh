@@ -3,7 +3,7 @@
 // triangle of A walks B's tree depth-first, nearer child first, pruning
 // against ONE shared monotone bound (the float32 bound cell of the engine,
 // slack E included), and counts every node it pops.  Leaves feed the same
-// band / exact pass as the front engine (k_bandsel, k_refine), so the answer
+// band / exact pass as the front engine (k_refine), so the answer
 // is the reference's exact distance and lexicographic witness.
 #pragma once
 
@@ -44,9 +44,8 @@ __global__ void k_dfs_init(QArgs q) {
   S->done = 0;
   S->err = 0;
   S->iter = 0;
-  S->leaf_buf = 1;  // k_bandsel's selection goes to node[1]
+  S->leaf_buf = 1;
   S->n_band = 0;
-  S->n_sel = 0;
   S->fbest = kMax ? 0u : __float_as_uint(INFINITY);
   S->expanded = 0;
   S->narrow = 0;

@@ -56,7 +56,6 @@ struct alignas(16) QState {
   int leaf_buf;                      // buffer holding the leaf-pair list
   unsigned long long n_in, n_out, n_leaf, n_band;
   unsigned long long n_cand;         // triangle-pair candidates (k_nfilter)
-  unsigned long long n_sel;          // band entries selected for the exact pass
   unsigned long long expanded, narrow, culled, band_eval;
   long long ov_cand, ov_in, ov_cap;
   float slack;

@@ -259,42 +259,15 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
 template <bool kMax>
 __device__ void finalize(const QArgs& q);
 
-// Exact pass, step 1 (k_bandsel).  Band entries whose float32 distance f is
-// within E of the best float32 distance f_best (S->fbest, tracked where the
-// band is filled) can still attain the exact optimum: |f - exact| <= E/2 for
-// every pair, so an entry with f > f_best + E is exactly worse than the
-// f_best pair (min query; mirrored for max).  Survivors are compacted into
-// the (now idle) leaf-pair buffer so step 2 can spread them evenly.
-template <bool kMax>
-__global__ __launch_bounds__(256) void k_bandsel(QArgs q) {
-  QState* S = q.S;
-  const unsigned long long n = min(S->n_band, q.band_cap);
-  const float E = S->slack;
-  const float fb = __uint_as_float(*reinterpret_cast<volatile unsigned*>(&S->fbest));
-  uint2* sel = q.node[S->leaf_buf];
-  const int lane = threadIdx.x & 31;
-  for (unsigned long long base = (unsigned long long)blockIdx.x * 256; base < n; base += gridDim.x * 256ull) {
-    const unsigned long long i = base + threadIdx.x;
-    bool cand = false;
-    if (i < n) {
-      const float f = q.band_d[i];
-      cand = kMax ? (f >= fb - E) : (f <= fb + E);  // +-inf (warm pair) always passes
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, cand);
-    unsigned long long wbase = 0;
-    if (lane == 0 && m) wbase = atomicAdd(&S->n_sel, (unsigned long long)__popc(m));
-    wbase = __shfl_sync(0xffffffffu, wbase, 0);
-    if (cand) {
-      const unsigned long long slot = wbase + __popc(m & ((1u << lane) - 1));
-      if (slot < q.cap) sel[slot] = q.band_ids[i];
-    }
-  }
-}
-
-// Exact pass, step 2 (k_refine): one thread per selected pair (exact_key),
-// lexicographic 128-bit minimum; the last block to finish writes the witness
-// and the result record.  Small blocks: the selection is a few thousand to a
-// few ten thousand pairs, each a long float64 dependency chain.
+// Exact pass (k_refine): one thread per band entry.  Entries whose float32
+// distance f is more than E from the best float32 distance f_best (S->fbest,
+// tracked where the band is filled) are skipped: |f - exact| <= E/2 for every
+// pair, so such an entry is exactly worse than the f_best pair (min query;
+// mirrored for max).  The rest are re-evaluated in the reference's
+// arithmetic (exact_key) and reduced to the lexicographic 128-bit minimum;
+// the last block to finish writes the witness and the result record.  The
+// grid has far more threads than a band has entries, so the skipped entries
+// cost one load each and no compaction pass is needed.
 constexpr int kRefineThreads = 64;
 
 template <bool kMax>
@@ -302,8 +275,9 @@ template <bool kMax>
 // 4 blocks / SM: 41 -> 36 us on the rings); max is short and stays at 12
 __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : 4) void k_refine(QArgs q) {
   QState* S = q.S;
-  const unsigned long long n = min(S->n_sel, q.cap);
-  const uint2* sel = q.node[S->leaf_buf];
+  const unsigned long long n = min(S->n_band, q.band_cap);
+  const float E = S->slack;
+  const float fb = __uint_as_float(*reinterpret_cast<volatile unsigned*>(&S->fbest));
   __shared__ Key128 wk[kRefineThreads / 32];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -313,7 +287,9 @@ __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : 4) void k_refine(QArgs 
   unsigned long long evals = 0;
   for (unsigned long long j = (unsigned long long)blockIdx.x * kRefineThreads + threadIdx.x; j < n;
        j += (unsigned long long)gridDim.x * kRefineThreads) {
-    const uint2 ids = sel[j];
+    const float f = q.band_d[j];
+    if (!(kMax ? f >= fb - E : f <= fb + E)) continue;  // +-inf (warm pair) always passes
+    const uint2 ids = q.band_ids[j];
     const Key128 k = exact_key<kMax>(q, ids.x, ids.y);
     if (key_less(k, best)) best = k;
     ++evals;

@@ -10,10 +10,10 @@
 //   k_ntest           float32 narrow phase on the candidates (min), fills the
 //                     exact-pass band
 //   k_nfilter<rescan> exits at once unless the band / candidate list overflowed
-//   k_bandsel         band entries within E of the best float32 distance
-//   k_refine          exact narrow phase (reference arithmetic, 64 or 32 bit),
-//                     one thread per selected pair, lexicographic 128-bit key
-//                     minimum; its last block writes the witness and result
+//   k_refine          exact narrow phase (reference arithmetic, 64 or 32 bit)
+//                     on the band entries within E of the best float32
+//                     distance, one thread per entry, lexicographic 128-bit
+//                     key minimum; its last block writes the witness and result
 // The bound is a float32 cell carrying a slack E:
 // culling is conservative, so every pair that can attain the reference's
 // exact answer reaches the exact pass.
@@ -141,12 +141,11 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
   if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
   mark(3);
   k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
-  k_bandsel<kMax><<<sms, 256, 0, s>>>(q);
   k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
   mark(4);
   mark(5);
   GD_CUDA(cudaGetLastError());
-  count_launches(kMax ? 5 : 6);
+  count_launches(kMax ? 4 : 5);
 }
 
 static QArgs make_args(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
@@ -248,10 +247,9 @@ static void launch_dfs(const QArgs& q, cudaStream_t s) {
   const long long m = q.ma.m;
   if (m > 0) k_dfs<kMax><<<(unsigned)((m + kDfsThreads - 1) / kDfsThreads), kDfsThreads, 0, s>>>(q);
   k_dfs_check<<<1, 1, 0, s>>>(q.S);
-  k_bandsel<kMax><<<sms, 256, 0, s>>>(q);
   k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);
   GD_CUDA(cudaGetLastError());
-  count_launches(m > 0 ? 6 : 5);
+  count_launches(m > 0 ? 5 : 4);
 }
 
 void dfs_query(const GdMesh& ma, const GdMesh& mb, const GdBvh& b, const GdConfig& cfg, void* ws, size_t ws_bytes,

@@ -137,7 +137,6 @@ __device__ void init_query(const QArgs& q) {
   S->n_leaf = 0;
   S->n_band = 0;
   S->n_cand = 0;
-  S->n_sel = 0;
   for (int i = 0; i < kMaxIters; ++i) S->t_sweep[i] = 0;
   S->fbest = kMax ? 0u : __float_as_uint(INFINITY);
   S->expanded = 0;
