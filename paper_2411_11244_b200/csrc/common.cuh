@@ -112,6 +112,13 @@ __device__ __forceinline__ void atomic_max_pos(unsigned int* cell, float v) {
   atomicMax(cell, __float_as_uint(fmaxf(v, 0.0f)));
 }
 
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may be scheduled while
+// its predecessor in the stream drains; it waits here, before touching the
+// predecessor's results, until that grid has completed and its writes are
+// visible.  A no-op for a normal launch.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 128-bit lexicographic key (hi, lo) and an atomic minimum on it.
 struct alignas(16) Key128 {
   unsigned long long hi, lo;

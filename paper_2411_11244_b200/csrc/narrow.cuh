@@ -88,6 +88,7 @@ __device__ __forceinline__ bool axis_separated(const Tri<float>& a, const Tri<fl
 //    final bound is evaluated in the reference arithmetic right here.
 template <bool kMax, bool kRescan>
 __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
+  grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
   const unsigned long long n = S->n_leaf;
   if (n == 0) return;
@@ -202,6 +203,7 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
 // test on the dense candidate list; updates the bound and fills the band.
 template <bool kMax>
 __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
+  grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
   const unsigned long long n = min(S->n_cand, q.cap);
   if (n == 0) return;
@@ -274,6 +276,7 @@ template <bool kMax>
 // min: the lean float64 feature loop keeps ~150 registers live (no spills at
 // 4 blocks / SM: 41 -> 36 us on the rings); max is short and stays at 12
 __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : 4) void k_refine(QArgs q) {
+  grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
   const unsigned long long n = min(S->n_band, q.band_cap);
   const float E = S->slack;

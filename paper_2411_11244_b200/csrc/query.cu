@@ -105,6 +105,24 @@ int phase_ms(float* out, int n) {
   return k;
 }
 
+// launch `kernel` so it may be scheduled while the previous kernel of the
+// stream drains (programmatic dependent launch; the kernel starts with
+// grid_dependency_wait), hiding the launch gap between the query's kernels
+template <typename... Args>
+static void launch_pdl(void (*kernel)(Args...), unsigned grid, unsigned block, cudaStream_t s, QArgs q) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  GD_CUDA(cudaLaunchKernelEx(&cfg, kernel, q));
+}
+
 template <bool kMax>
 static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_done) {
   const int sms = num_sms();
@@ -137,11 +155,20 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
   // may start once this event has fired
   if (traversal_done) GD_CUDA(cudaEventRecord(traversal_done, s));
   mark(2);
-  k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
-  if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
-  mark(3);
-  k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
-  k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
+  // profiling events between the kernels would serialise them: PDL only
+  // when the phases are not being timed
+  if (g_profile) {
+    k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
+    if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
+    mark(3);
+    k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
+    k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
+  } else {
+    launch_pdl(k_nfilter<kMax, false>, sms * 8, 256, s, q);
+    if (!kMax) launch_pdl(k_ntest<kMax>, sms * 4, 256, s, q);
+    launch_pdl(k_nfilter<kMax, true>, sms, 256, s, q);
+    launch_pdl(k_refine<kMax>, sms * 16, kRefineThreads, s, q);
+  }
   mark(4);
   mark(5);
   GD_CUDA(cudaGetLastError());
