@@ -112,6 +112,22 @@ __device__ __forceinline__ void atomic_max_pos(unsigned int* cell, float v) {
   atomicMax(cell, __float_as_uint(fmaxf(v, 0.0f)));
 }
 
+// NaN-propagating float32 min / max (PTX min.NaN / max.NaN): the box
+// unions of numpy's np.minimum / np.maximum, which the reference's boxes use
+// (bvh.py:242-264) -- a NaN coordinate poisons every box above it, up to the
+// root, so a query over it culls everything and returns NaN as the
+// reference's does.  fminf / fmaxf would silently drop the NaN.
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float d;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
 // Programmatic dependent launch: a kernel launched with
 // cudaLaunchAttributeProgrammaticStreamSerialization may be scheduled while
 // its predecessor in the stream drains; it waits here, before touching the

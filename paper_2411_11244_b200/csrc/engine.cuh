@@ -130,8 +130,8 @@ __device__ __forceinline__ Box box_union(const Box& a, const Box& b) {
   Box r;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    r.lo[k] = fminf(a.lo[k], b.lo[k]);
-    r.hi[k] = fmaxf(a.hi[k], b.hi[k]);
+    r.lo[k] = fmin_nan(a.lo[k], b.lo[k]);
+    r.hi[k] = fmax_nan(a.hi[k], b.hi[k]);
   }
   return r;
 }

@@ -36,8 +36,8 @@ __device__ __forceinline__ Box shfl_union(const Box& b, int o, unsigned mask) {
   Box r;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    r.lo[k] = fminf(b.lo[k], __shfl_down_sync(mask, b.lo[k], o));
-    r.hi[k] = fmaxf(b.hi[k], __shfl_down_sync(mask, b.hi[k], o));
+    r.lo[k] = fmin_nan(b.lo[k], __shfl_down_sync(mask, b.lo[k], o));
+    r.hi[k] = fmax_nan(b.hi[k], __shfl_down_sync(mask, b.hi[k], o));
   }
   return r;
 }
@@ -95,12 +95,12 @@ __device__ __forceinline__ Box load_box_cg(const float* box, unsigned long long 
 }
 
 __device__ __forceinline__ void grow(Box& b, const V3<float>& p) {
-  b.lo[0] = fminf(b.lo[0], p.x);
-  b.lo[1] = fminf(b.lo[1], p.y);
-  b.lo[2] = fminf(b.lo[2], p.z);
-  b.hi[0] = fmaxf(b.hi[0], p.x);
-  b.hi[1] = fmaxf(b.hi[1], p.y);
-  b.hi[2] = fmaxf(b.hi[2], p.z);
+  b.lo[0] = fmin_nan(b.lo[0], p.x);
+  b.lo[1] = fmin_nan(b.lo[1], p.y);
+  b.lo[2] = fmin_nan(b.lo[2], p.z);
+  b.hi[0] = fmax_nan(b.hi[0], p.x);
+  b.hi[1] = fmax_nan(b.hi[1], p.y);
+  b.hi[2] = fmax_nan(b.hi[2], p.z);
 }
 
 // One launch refits the whole tree.  Each block: leaf boxes from the streamed
@@ -272,8 +272,8 @@ __global__ void k_export_leaf(GdMesh m, GdBvh B, T* nmin, T* nmax) {
       if (c == 0) {
         lo[k] = hi[k] = x[k];
       } else {
-        lo[k] = x[k] < lo[k] ? x[k] : lo[k];
-        hi[k] = x[k] > hi[k] ? x[k] : hi[k];
+        lo[k] = (x[k] < lo[k] || x[k] != x[k]) ? x[k] : lo[k];  // np.min: NaN wins
+        hi[k] = (x[k] > hi[k] || x[k] != x[k]) ? x[k] : hi[k];
       }
     }
   }
@@ -291,9 +291,9 @@ __global__ void k_export_level(T* nmin, T* nmax, int lv) {
   const long long node = ((1ll << lv) - 1) + r, c0 = 2 * node + 1, c1 = c0 + 1;
   for (int k = 0; k < 3; ++k) {
     const T a = nmin[3 * c0 + k], b = nmin[3 * c1 + k];
-    nmin[3 * node + k] = b < a ? b : a;  // np.minimum
+    nmin[3 * node + k] = (b < a || b != b) ? b : a;  // np.minimum (a NaN operand wins)
     const T c = nmax[3 * c0 + k], d = nmax[3 * c1 + k];
-    nmax[3 * node + k] = d > c ? d : c;  // np.maximum
+    nmax[3 * node + k] = (d > c || d != d) ? d : c;  // np.maximum
   }
 }
 

@@ -122,8 +122,15 @@ __device__ void init_query(const QArgs& q) {
   const float E = M * 0x1p-15f;
   S->slack = E;
   const float key0 = pair_key<kMax>(ra, rb);  // squared
-  const float b0 = sqrtf(pair_update<kMax>(ra, rb, q.cfg.enhanced_bounds != 0));
-  S->bound_bits = __float_as_uint(kMax ? fmaxf(b0 - E, 0.f) : b0 + E);
+  bool nan_root = false;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    nan_root = nan_root || ra.lo[k] != ra.lo[k] || ra.hi[k] != ra.hi[k] || rb.lo[k] != rb.lo[k] || rb.hi[k] != rb.hi[k];
+  const float b0 = nan_root ? __int_as_float(0x7fc00000) : sqrtf(pair_update<kMax>(ra, rb, q.cfg.enhanced_bounds != 0));
+  // a NaN root box (a NaN vertex, propagated by the refit) leaves a NaN
+  // bound: every candidate is culled and the distance is NaN, as in the
+  // reference (its np.minimum boxes and `key < bound` tests)
+  S->bound_bits = __float_as_uint(kMax ? (b0 != b0 ? b0 : fmaxf(b0 - E, 0.f)) : b0 + E);
   S->best.hi = ~0ull;
   S->best.lo = ~0ull;
   S->done = 0;

@@ -338,3 +338,41 @@ def test_deformed_meshes(md, gpu, oracle):
         a.deformed(torch.zeros((3, 3), dtype=torch.float64, device="cuda"))
     with pytest.raises(ValueError):
         a.deformed(np.zeros((a.n_vertices + 1, 3)))
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_nonfinite_vertices(md, gpu, oracle, prec):
+    """Non-finite coordinates behave as in the reference (its np.minimum /
+    np.maximum boxes propagate NaN to the root; `key < nan` culls every
+    candidate): a NaN vertex gives distance NaN, no witness, one iteration
+    that culls the root's whole expansion; +-inf coordinates give the
+    brute-force minimum and an infinite maximum without a witness (the
+    reference's values on this scene, checked here in CPU tests' terms)."""
+    import warnings
+
+    warnings.simplefilter("ignore")
+    dt = np.float64 if prec == 64 else np.float32
+    cfg = md.EngineConfig(precision=prec)
+    a, b = md.gen_scene("random-blobs", {"n": 50, "seed": 1})
+    for side in ("a", "b"):
+        V = (a if side == "a" else b).vertices.copy()
+        V[5] = np.nan
+        bad = md.TriangleMesh(V, (a if side == "a" else b).triangles)
+        ma, mb = (bad, b) if side == "a" else (a, bad)
+        ta, tb = md.build_f12(ma, dtype=dt), md.build_f12(mb, dtype=dt)
+        assert np.isnan((ta if side == "a" else tb).node_min[0]).all()
+        for run in (md.run_min_query, md.run_max_query):
+            r = run(ma, mb, ta, tb, cfg)
+            assert np.isnan(r.distance) and r.witness is None, (side, run.__name__)
+            assert len(r.iterations) == 1 and r.iterations[0].front_out == 0
+            assert r.iterations[0].culled == 4 ** r.iterations[0].k == r.expanded_pairs and r.narrow_pairs == 0
+    for val in (np.inf, -np.inf):
+        V = a.vertices.copy()
+        V[5, 1] = val
+        a2 = md.TriangleMesh(V, a.triangles)
+        ta, tb = md.build_f12(a2, dtype=dt), md.build_f12(b, dtype=dt)
+        r = md.run_min_query(a2, b, ta, tb, cfg)
+        d, ia, ib, _, _ = oracle.brute_force(a2.triangle_points(dt), b.triangle_points(dt), "min")
+        assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (ia, ib)
+        r = md.run_max_query(a2, b, ta, tb, cfg)
+        assert r.distance == np.inf and r.witness is None

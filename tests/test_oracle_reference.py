@@ -159,3 +159,33 @@ def test_load_obj_large_matches_reference(reference, md, tmp_path):
             fh.write(f"f {t[0] + 1} {t[1] + 1} {t[2] + 1}\n")
     got, want = md.load_obj(p), reference.load_obj(p)
     assert np.array_equal(got.vertices, want.vertices) and np.array_equal(got.triangles, want.triangles)
+
+
+def test_reference_nonfinite_semantics(reference):
+    """Pins the behaviour tests/test_gpu_parity.py::test_nonfinite_vertices
+    asserts for the device engine: a NaN vertex makes the reference's root box
+    NaN (np.minimum), every candidate is culled and the distance is NaN with
+    no witness after one iteration; +-inf gives a finite minimum and an
+    infinite, witness-less maximum."""
+    import warnings
+
+    warnings.simplefilter("ignore")
+    a, b = reference.gen_scene("random-blobs", {"n": 50, "seed": 1})
+    V = a.vertices.copy()
+    V[5] = np.nan
+    a2 = reference.TriangleMesh(V, a.triangles)
+    ta, tb = reference.build_f12(a2), reference.build_f12(b)
+    assert np.isnan(ta.node_min[0]).all()
+    for run in (reference.run_min_query, reference.run_max_query):
+        r = run(a2, b, ta, tb)
+        assert np.isnan(r.distance) and r.witness is None and len(r.iterations) == 1
+        s = r.iterations[0]
+        assert s.front_out == 0 and s.culled == 4 ** s.k == r.expanded_pairs and r.narrow_pairs == 0
+    V = a.vertices.copy()
+    V[5, 1] = np.inf
+    a3 = reference.TriangleMesh(V, a.triangles)
+    ta = reference.build_f12(a3)
+    rmin = reference.run_min_query(a3, b, ta, tb)
+    assert rmin.distance == reference.brute_force_min(a3, b)[0] and rmin.witness is not None
+    rmax = reference.run_max_query(a3, b, ta, tb)
+    assert rmax.distance == np.inf and rmax.witness is None
