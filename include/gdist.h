@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 10
+#define GDIST_ABI_VERSION 11
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -139,6 +139,15 @@ typedef struct GdConfig {
    * bound exactly as warm_a / warm_b do.  NULL = none.  Stream order makes
    * it safe: the producing query ran earlier on the same stream. */
   const void* warm_from;
+  /* bound sharing across the ranks of a split query: a
+   * DEVICE array of n_peers pointers to the other ranks' bound cells
+   * (gd_query_bound_device of their workspaces, mapped here through CUDA IPC
+   * -- NVLink peer memory).  Every bound this query commits is also applied
+   * to those cells with a system-scope atomicMin / atomicMax, so every rank
+   * culls with the best bound found anywhere.  0 / NULL = rank-local. */
+  const void* peer_bounds;
+  int32_t n_peers;
+  int32_t _pad2;
 } GdConfig;
 
 /* QueryResult (query.py:230-263) + Witness (query.py:136-144). */
@@ -255,6 +264,16 @@ int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a
 /* Device address of the result record inside a query workspace (valid
  * after a query on that workspace completes in stream order). */
 int gd_query_result_device(const GdConfig* cfg, void* workspace, const void** out);
+/* Device address of the bound cell inside a query workspace (the target of
+ * the peers' GdConfig.peer_bounds). */
+int gd_query_bound_device(const GdConfig* cfg, void* workspace, void** out);
+/* CUDA IPC for the bound exchange: the handle (64 bytes) of the allocation
+ * holding `ptr` and ptr's offset in it; open maps a peer's handle into this
+ * process (peer access enabled lazily) and returns base + offset; close
+ * unmaps (pass the base, i.e. the opened pointer minus the offset). */
+int gd_ipc_handle(const void* ptr, void* handle_out, uint64_t* offset);
+int gd_ipc_open(const void* handle, uint64_t offset, void** ptr_out);
+int gd_ipc_close(void* base);
 int gd_query_result_async(const GdConfig* cfg, void* workspace, void* host_dst, int max_stats, void* stream);
 int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* workspace,
                      const GdResult* result_dev, GdResult* out, GdIterStat* stats, int max_stats,

@@ -86,6 +86,9 @@ class GdConfig(C.Structure):
         ("split_level", C.c_int32),
         ("frame", C.c_int32),
         ("warm_from", C.c_void_p),
+        ("peer_bounds", C.c_void_p),
+        ("n_peers", C.c_int32),
+        ("_pad2", C.c_int32),
     ]
 
 
@@ -146,6 +149,10 @@ _SIGNATURES = {
     "gd_query_async_ev": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
                                     C.POINTER(GdConfig), P, C.c_size_t, P, P, P]),
     "gd_query_result_device": (C.c_int, [C.POINTER(GdConfig), P, C.POINTER(C.c_void_p)]),
+    "gd_query_bound_device": (C.c_int, [C.POINTER(GdConfig), P, C.POINTER(C.c_void_p)]),
+    "gd_ipc_handle": (C.c_int, [P, P, C.POINTER(C.c_uint64)]),
+    "gd_ipc_open": (C.c_int, [P, C.c_uint64, C.POINTER(C.c_void_p)]),
+    "gd_ipc_close": (C.c_int, [P]),
     "gd_query_result_async": (C.c_int, [C.POINTER(GdConfig), P, P, C.c_int, P]),
     "gd_query_collect": (C.c_int, [C.POINTER(GdBvh), C.POINTER(GdBvh), C.POINTER(GdConfig), P, P,
                                    C.POINTER(GdResult), C.POINTER(GdIterStat), C.c_int, P]),

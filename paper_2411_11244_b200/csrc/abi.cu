@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstring>
 #include <string>
 
 #include "engine.cuh"
@@ -29,6 +30,7 @@ size_t query_workspace_size(const GdConfig& cfg);
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done);
 const void* query_result_device(const GdConfig& cfg, void* ws);
+void* query_bound_device(const GdConfig& cfg, void* ws);
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
 void query_collect(const GdConfig& cfg, void* ws, const GdResult* result_dev, GdResult* out, GdIterStat* stats,
                    int max_stats, cudaStream_t s);
@@ -221,6 +223,54 @@ int gd_query_result_device(const GdConfig* cfg, void* workspace, const void** ou
     GD_CHECK(cfg && workspace && out, GD_ERR_INVALID, "null argument");
     *out = query_result_device(*cfg, workspace);
   });
+}
+
+int gd_query_bound_device(const GdConfig* cfg, void* workspace, void** out) {
+  return guarded([&] {
+    GD_CHECK(cfg && workspace && out, GD_ERR_INVALID, "null argument");
+    *out = query_bound_device(*cfg, workspace);
+  });
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no libcuda
+// link dependency): the base of the allocation a pointer lies in
+typedef int (*AddressRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+int gd_ipc_handle(const void* ptr, void* handle_out, uint64_t* offset) {
+  return guarded([&] {
+    GD_CHECK(ptr && handle_out && offset, GD_ERR_INVALID, "null argument");
+    static AddressRangeFn range = nullptr;
+    if (!range) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      GD_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+      GD_CHECK(fn && q == cudaDriverEntryPointSuccess, GD_ERR_CUDA, "cuMemGetAddressRange unavailable");
+      range = reinterpret_cast<AddressRangeFn>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    GD_CHECK(range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) == 0, GD_ERR_CUDA,
+             "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    GD_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    memcpy(handle_out, &h, sizeof h);
+    *offset = reinterpret_cast<unsigned long long>(ptr) - base;
+  });
+}
+
+int gd_ipc_open(const void* handle, uint64_t offset, void** ptr_out) {
+  return guarded([&] {
+    GD_CHECK(handle && ptr_out, GD_ERR_INVALID, "null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void* base = nullptr;
+    GD_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr_out = static_cast<char*>(base) + offset;
+  });
+}
+
+int gd_ipc_close(void* base) {
+  return guarded([&] { GD_CUDA(cudaIpcCloseMemHandle(base)); });
 }
 
 int gd_query_collect(const GdBvh* a, const GdBvh* b, const GdConfig* cfg, void* workspace, const GdResult* result_dev,

@@ -189,7 +189,7 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   if (kMax && !kRescan) {
     upd = warp_max(upd);
     if (lane == 0 && upd > 0.f) {
-      commit_bound<kMax>(S, upd);
+      commit_bound<kMax>(q, upd);
       atomicMax(&S->fbest, __float_as_uint(upd));
     }
   }
@@ -245,7 +245,7 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
     float u = warp_upd[0];
     for (int w = 1; w < 8; ++w) u = kMax ? fmaxf(u, warp_upd[w]) : fminf(u, warp_upd[w]);
     if (kMax ? u > 0.f : u < INFINITY) {
-      commit_bound<kMax>(S, u);
+      commit_bound<kMax>(q, u);
       if (kMax)
         atomicMax(&S->fbest, __float_as_uint(u));
       else

@@ -62,6 +62,8 @@ static void validate(const GdBvh& a, const GdBvh& b, const GdConfig& cfg) {
   GD_CHECK(cfg.depth_cap >= 1 && cfg.depth_cap <= 16, GD_ERR_CONFIG, "depth_cap must be in [1, 16]");
   GD_CHECK(cfg.front_hard_cap >= 4, GD_ERR_CONFIG, "front_hard_cap must be >= 4");
   GD_CHECK(cfg.frame == 0 || cfg.frame == 1, GD_ERR_CONFIG, "frame must be 0 (world) or 1 (B-local)");
+  GD_CHECK(cfg.n_peers >= 0 && cfg.n_peers <= 64 && (cfg.n_peers == 0 || cfg.peer_bounds), GD_ERR_INVALID,
+           "peer_bounds must list n_peers (<= 64) bound cells");
   GD_CHECK(a.depth >= 0 && a.depth <= 31 && b.depth >= 0 && b.depth <= 31, GD_ERR_INVALID,
            "tree depth out of range");
   GD_CHECK(a.box && b.box && a.leaf_rec && b.leaf_rec && a.vtx32 && b.vtx32 && a.vmap && b.vmap,
@@ -229,6 +231,11 @@ static_assert(offsetof(QState, stats) == offsetof(QState, res) + sizeof(GdResult
 const void* query_result_device(const GdConfig& cfg, void* ws) {
   WsLayout L = ws_layout(cfg);
   return &reinterpret_cast<const QState*>(static_cast<char*>(ws) + L.state)->res;
+}
+
+void* query_bound_device(const GdConfig& cfg, void* ws) {
+  WsLayout L = ws_layout(cfg);
+  return &reinterpret_cast<QState*>(static_cast<char*>(ws) + L.state)->bound_bits;
 }
 
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s) {

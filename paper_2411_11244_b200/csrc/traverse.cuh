@@ -35,6 +35,24 @@ __device__ __forceinline__ void commit_bound(QState* S, float v) {
   else
     atomic_min_pos(&S->bound_bits, v + S->slack);
 }
+// the same, also applied to the other ranks' bound cells of a split query
+// (GdConfig.peer_bounds: their workspaces mapped over NVLink).  A bound is an
+// achieved distance +- the common slack, valid for every rank's sub-query.
+template <bool kMax>
+__device__ __forceinline__ void commit_bound(const QArgs& q, float v) {
+  QState* S = q.S;
+  commit_bound<kMax>(S, v);
+  if (q.cfg.n_peers > 0) {
+    const unsigned bits = __float_as_uint(fmaxf(kMax ? v - S->slack : v + S->slack, 0.f));
+    unsigned* const* peers = static_cast<unsigned* const*>(q.cfg.peer_bounds);
+    for (int i = 0; i < q.cfg.n_peers; ++i) {
+      if (kMax)
+        atomicMax_system(peers[i], bits);
+      else
+        atomicMin_system(peers[i], bits);
+    }
+  }
+}
 
 // Keys and bound updates are kept SQUARED inside the traversal (no sqrt per
 // candidate); the bound cell itself is a distance, squared once per tile.
@@ -402,7 +420,7 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
         sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
         float u = sh.warp_upd[0];
         for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
-        if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
+        if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u));
       }
       __syncthreads();
       const unsigned total = sh.stage_count;
@@ -467,7 +485,7 @@ __device__ __forceinline__ void expand_sweep(const QArgs& q, ExpandShared& sh, u
         sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
         float u = sh.warp_upd[0];
         for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[w]) : fminf(u, sh.warp_upd[w]);
-        if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(S, sqrtf(u));
+        if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u));
       }
       __syncthreads();
       unsigned long long slot = sh.out_base + my_off;

@@ -12,7 +12,12 @@ query.py:426-433 parallelises only over CPU threads).
   part independently -- its own bound is a valid global bound, so every pair
   that can attain the optimum survives on its owner -- and the exact answers
   are combined with the reference's lexicographic witness rule
-  (query.py:205-220) in one all-gather.
+  (query.py:205-220) in one all-gather.  With `share_bound` (the default when the
+  ranks share a node) the ranks' bound cells are mapped into each other over
+  CUDA IPC (NVLink peer memory) and every bound a rank commits is applied to
+  all of them with a system-scope atomic, inside the kernels -- the
+  per-round bound exchange of SURVEY.md 8(e) without a host round trip, so
+  every rank culls with the best bound found anywhere.
 
 The collective plumbing is torch.distributed (NCCL on GPUs, gloo in the CPU
 tests); the per-frame / per-part compute is libgdist's.
@@ -200,28 +205,109 @@ def combine_parts(kind: str, parts: list) -> tuple:
     return min(found, key=lambda p: (-p[0], p[1], p[2]))
 
 
-def run_split_query(mesh_a, mesh_b, bvh_a, bvh_b, kind: str = "min", cfg=None, group=None, split_level: int = 5,
-                    rank: int | None = None, world: int | None = None):
+_SPLIT_PLANS: dict = {}
+
+
+def _link_bounds(pq, rank: int, world: int, group=None):
+    """Map every rank's bound cell into this rank (CUDA IPC; collective over
+    `group`) and point this plan's GdConfig.peer_bounds at the others'."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+
+    dist = _dist()
+    L = _lib.lib()
+    cell = C.c_void_p()
+    _lib.check(L.gd_query_bound_device(C.byref(pq.g_cfg), _lib.ptr(pq.ws), C.byref(cell)), "query_bound_device")
+    handle = (C.c_char * 64)()
+    off = C.c_uint64()
+    _lib.check(L.gd_ipc_handle(cell, handle, C.byref(off)), "ipc_handle")
+    mine = (rank, bytes(handle), int(off.value))
+    objs = [None] * world
+    dist.all_gather_object(objs, mine, group=group)
+    peers, opened = [], []
+    for r, h, o in sorted(objs):
+        if r == rank:
+            continue
+        ptr = C.c_void_p()
+        _lib.check(L.gd_ipc_open((C.c_char * 64).from_buffer_copy(h), o, C.byref(ptr)), "ipc_open")
+        peers.append(ptr.value)
+        opened.append(ptr.value - o)
+    arr = torch.tensor(peers, dtype=torch.int64, device=torch.device("cuda", torch.cuda.current_device()))
+    pq._peer_arr, pq._peer_bases = arr, opened
+    pq.g_cfg.peer_bounds = arr.data_ptr()
+    pq.g_cfg.n_peers = len(peers)
+
+
+def _split_plan(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level, group):
+    """The cached per-rank plan of a bound-sharing split query (private
+    workspace whose bound cell is linked to the other ranks' once)."""
+    from .query import PreparedQuery
+
+    key = (id(bvh_a), id(bvh_b), cfg, kind, rank, world, split_level, id(group))
+    ent = _SPLIT_PLANS.get(key)
+    if ent is None or ent[0] is not bvh_a or ent[1] is not bvh_b:
+        pq = PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, private_workspace=True)
+        pq.g_cfg.split_rank, pq.g_cfg.split_world, pq.g_cfg.split_level = int(rank), int(world), int(split_level)
+        _link_bounds(pq, rank, world, group)
+        ent = (bvh_a, bvh_b, pq)
+        _SPLIT_PLANS[key] = ent
+    return ent[2].bind(mesh_a, mesh_b)
+
+
+def release_split_plans(group=None):
+    """Drop the bound-linked split plans and their workspaces (collective:
+    after a barrier no rank writes into another's bound cell any more).
+    Linked plans are kept until then -- a peer may still hold a mapping of
+    their bound cells."""
+    from . import _lib
+
+    dist = _dist()
+    if dist.is_available() and dist.is_initialized():
+        _lib.torch().cuda.synchronize()
+        dist.barrier(group=group)
+    for _, _, pq in list(_SPLIT_PLANS.values()):
+        for base in getattr(pq, "_peer_bases", []):
+            _lib.lib().gd_ipc_close(base)
+    _SPLIT_PLANS.clear()
+
+
+def run_split_query(mesh_a, mesh_b, bvh_a, bvh_b, kind: str = "min", cfg=None, group=None, split_level: int | None = None,
+                    rank: int | None = None, world: int | None = None, share_bound: bool = False):
     """One query split over the ranks of `group` (or, with explicit
     rank / world, one part of it -- e.g. to emulate the split on one GPU).
 
     Each rank expands only the node pairs whose ancestor pair at tree level
     `split_level` hashes to it (gdist.h GdConfig.split_*), and the exact
-    per-rank answers are combined with the reference's witness rule.  The
-    returned QueryResult carries the global distance / witness and this
-    rank's own iteration statistics."""
+    per-rank answers are combined with the reference's witness rule.  With
+    `share_bound` (and a process group spanning the ranks) the ranks' bound
+    cells are linked over CUDA IPC / NVLink (GdConfig.peer_bounds), so each
+    part culls with the global best bound.  The returned QueryResult carries
+    the global distance / witness and this rank's own iteration statistics.
+    Collective: every rank of the group calls it with the same arguments."""
     import torch
 
     from .query import EngineConfig, QueryResult, Witness
 
-    if rank is None or world is None:
+    dist = _dist()
+    grouped = rank is None or world is None
+    if grouped:
         rank, world = world_info(group)
-    r = split_part(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg or EngineConfig(), rank, world, split_level)
+    cfg = cfg or EngineConfig()
+    if split_level is None:
+        split_level = default_split_level(bvh_a, bvh_b)
+    if share_bound and grouped and world > 1:
+        # every rank has finished its previous split query (the all-gather
+        # below), so no peer cell is still in use by another query
+        r = _split_plan(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level, group).run()
+    else:
+        r = split_part(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level)
     w = r.witness
     mine = torch.tensor([r.distance, -1.0 if w is None else w.tri_a, -1.0 if w is None else w.tri_b,
                          *(w.point_a if w is not None else np.zeros(3)), *(w.point_b if w is not None else np.zeros(3))],
                         dtype=torch.float64)
-    dist = _dist()
     if world > 1 and dist.is_available() and dist.is_initialized() and world == dist.get_world_size(group):
         dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else mine.device
         out = torch.empty(world * mine.numel(), dtype=torch.float64, device=dev)
@@ -236,11 +322,20 @@ def run_split_query(mesh_a, mesh_b, bvh_a, bvh_b, kind: str = "min", cfg=None, g
     return QueryResult(kind, best[0], wit, r.iterations, r.expanded_pairs, r.narrow_pairs, band_pairs=r.band_pairs)
 
 
-def split_part(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank: int, world: int, split_level: int = 5):
+def default_split_level(bvh_a, bvh_b) -> int:
+    """Tree level whose ancestor pairs deal the work: 11 (4M ancestor pairs,
+    the best balance measured on the rings / shells), at
+    least 3 levels above the shallower tree's leaves."""
+    return max(1, min(11, min(bvh_a.depth, bvh_b.depth) - 3))
+
+
+def split_part(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank: int, world: int, split_level: int | None = None):
     """This rank's part of a split query: its exact best over the node pairs
     it owns (QueryResult with the part's own witness and statistics)."""
     from .query import PreparedQuery
 
+    if split_level is None:
+        split_level = default_split_level(bvh_a, bvh_b)
     pq = PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind)
     pq.g_cfg.split_rank, pq.g_cfg.split_world, pq.g_cfg.split_level = int(rank), int(world), int(split_level)
     return pq.run()

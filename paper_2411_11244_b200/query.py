@@ -267,7 +267,7 @@ def _gd_config(cfg: EngineConfig, kind: str, warm_pair, band_cap: int = 0) -> _l
     else:
         g.warm_a = g.warm_b = -1
     g.band_cap = band_cap
-    g.split_rank, g.split_world, g.split_level = 0, 1, 5
+    g.split_rank, g.split_world, g.split_level = 0, 1, 11
     return g
 
 

@@ -1,7 +1,8 @@
 """Multi-GPU paths on one GPU (gpurun provides one): the split query's parts
 run one after another and combine to the single-GPU answer; two processes
-sharing cuda:0 over a gloo group run the distributed split query and the
-sharded frame sequence end to end."""
+sharing cuda:0 over a gloo group run the distributed split query (with the
+ranks' bound cells linked over CUDA IPC, and without) and the sharded frame
+sequence end to end."""
 
 import os
 import socket
@@ -64,12 +65,17 @@ def _worker(rank, world, port, q):
         ta, tb = md.build_f12(a), md.build_f12(b)
         out = {}
         for kind in ("min", "max"):
-            r = md.run_split_query(a, b, ta, tb, kind)
-            out[kind] = (r.distance, r.witness.tri_a, r.witness.tri_b, r.witness.point_a.tolist())
+            for rep in range(2):  # the linked plan is cached: the second call reuses the IPC mapping
+                r = md.run_split_query(a, b, ta, tb, kind, share_bound=True)  # bound cells linked over CUDA IPC
+                out[kind] = (r.distance, r.witness.tri_a, r.witness.tri_b, r.witness.point_a.tolist())
+            loc = md.run_split_query(a, b, ta, tb, kind, share_bound=False)
+            out[kind + "_local"] = (loc.distance, loc.witness.tri_a, loc.witness.tri_b, loc.witness.point_a.tolist())
+            out[kind + "_work"] = (r.expanded_pairs, loc.expanded_pairs)
         tz, tbase = md.ring_pair_base(60, 30)
         za, zb = md.build_f12(tz), md.build_f12(tbase)
         xfs = [md.ring_frame_transforms(f) for f in range(0, 70, 10)]
         seq = md.run_sequence(tz, tbase, za, zb, xfs, "min")
+        md.parallel.release_split_plans()
         q.put((rank, out, seq.tolist()))
     finally:
         dist.destroy_process_group()
@@ -111,6 +117,7 @@ def test_two_processes_gloo(md, gpu):
             r = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb)
             assert out[kind][:3] == (r.distance, r.witness.tri_a, r.witness.tri_b), (rank, kind)
             assert out[kind][3] == r.witness.point_a.tolist()
+            assert out[kind + "_local"] == out[kind], (rank, kind)
         assert np.array_equal(np.asarray(seq), np.asarray(want_seq, dtype=np.float64)), rank
 
 
