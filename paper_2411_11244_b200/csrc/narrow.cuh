@@ -109,6 +109,9 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
     const float ub = load_bound(S), ub2 = ub * ub;
     unsigned mask = 0;
     uint2 lp = make_uint2(0, 0);
+    float dd[4] = {-1.f, -1.f, -1.f, -1.f};  // max: float32 distances of the tested pairs
+    unsigned tid[4] = {0u, 0u, 0u, 0u};     // max: their (tri_a, tri_b) halves, packed below
+    unsigned tib[4] = {0u, 0u, 0u, 0u};
     if (i < n && (!culling || survives<kMax>(keys[i], ub2))) {
       lp = leaves[i];
       const LeafRec ra = load_leaf(q.A, lp.x), rb = load_leaf(q.B, lp.y);
@@ -143,23 +146,52 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
                                  : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr));
             if (kMax) upd = fmaxf(upd, d);
             ++tested;
-            if (kMax ? (d + E >= ub) : (d - E <= ub)) {
-              if (kRescan) {
+            if (kRescan) {
+              if (kMax ? (d + E >= ub) : (d - E <= ub))
                 atomic_min_key(&S->best, exact_key<kMax>(q, ra.tri_id(ia), rb.tri_id(ib)));
-              } else {
-                const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
-                if (slot < q.band_cap) {
-                  q.band_ids[slot] = make_uint2(ra.tri_id(ia), rb.tri_id(ib));
-                  q.band_d[slot] = d;
-                } else {
-                  S->band_overflow = 1;
-                }
-              }
+            } else {
+              // max: appended below, warp-aggregated
+              dd[2 * ia + ib] = d;
+              tid[2 * ia + ib] = ra.tri_id(ia);
+              tib[2 * ia + ib] = rb.tri_id(ib);
             }
           } else {
             mask |= 1u << (2 * ia + ib);
           }
         }
+    }
+    if (kMax && !kRescan) {
+      // band append, one reservation per warp.  Besides the bound test, a
+      // pair more than E below the warp's best float32 distance cannot be the
+      // answer (fbest >= that best; k_refine skips f < fbest - E) and stays out
+      const float thr = fmaxf(ub, warp_max(upd)) - E;
+      unsigned m4 = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (dd[c] >= 0.f && dd[c] >= thr) m4 |= 1u << c;
+      const unsigned cnt = __popc(m4);
+      unsigned incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      unsigned long long wbase = 0;
+      if (lane == 31 && incl) wbase = atomicAdd(&S->n_band, (unsigned long long)incl);
+      wbase = __shfl_sync(0xffffffffu, wbase, 31);
+      unsigned long long pos = wbase + incl - cnt;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (m4 & (1u << c)) {
+          if (pos < q.band_cap) {
+            q.band_ids[pos] = make_uint2(tid[c], tib[c]);
+            q.band_d[pos] = dd[c];
+          } else {
+            S->band_overflow = 1;  // the rescan pass covers every leaf pair
+          }
+          ++pos;
+        }
+      }
     }
     if (!kMax && !kRescan) {
       // warp-aggregated append of up to 4 triangle pairs per thread
@@ -214,20 +246,36 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   __shared__ float warp_upd[8];
   float upd = kMax ? 0.f : INFINITY;
   unsigned long long tested = 0;
-  for (unsigned long long j = blockIdx.x * 256ull + threadIdx.x; j < n; j += gridDim.x * 256ull) {
-    ++tested;
-    const uint2 c = cand[j];
-    const LeafRec ra = load_leaf(q.A, c.x >> 1), rb = load_leaf(q.B, c.y >> 1);
-    const int ia = c.x & 1, ib = c.y & 1;
-    const Tri<float> A = leaf_tri32(q.A, xa, ra, ia), B = leaf_tri32(q.B, xb, rb, ib);
-    const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
-                         : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
-    upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
+  const int lane = threadIdx.x & 31;
+  // warp-uniform loop (the band append below is warp-aggregated)
+  for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
+    const unsigned long long j = base + threadIdx.x;
+    float d = kMax ? -1.f : INFINITY;
+    uint2 ids = make_uint2(0, 0);
+    if (j < n) {
+      ++tested;
+      const uint2 c = cand[j];
+      const LeafRec ra = load_leaf(q.A, c.x >> 1), rb = load_leaf(q.B, c.y >> 1);
+      const int ia = c.x & 1, ib = c.y & 1;
+      const Tri<float> A = leaf_tri32(q.A, xa, ra, ia), B = leaf_tri32(q.B, xb, rb, ib);
+      d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
+               : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+      upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
+      ids = make_uint2(ra.tri_id(ia), rb.tri_id(ib));
+    }
+    // band: within E of the bound, and within E of the warp's best float32
+    // distance (fbest is at least as good; k_refine drops the rest anyway)
     const float ub = load_bound(S);
-    if (kMax ? (d + E >= ub) : (d - E <= ub)) {
-      const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
+    const float wu = kMax ? warp_max(upd) : warp_min(upd);  // every lane: a full-warp shuffle
+    const bool app = j < n && (kMax ? d >= fmaxf(ub, wu) - E : d <= fminf(ub, wu) + E);
+    const unsigned m = __ballot_sync(0xffffffffu, app);
+    unsigned long long wbase = 0;
+    if (lane == 0 && m) wbase = atomicAdd(&S->n_band, (unsigned long long)__popc(m));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (app) {
+      const unsigned long long slot = wbase + __popc(m & ((1u << lane) - 1));
       if (slot < q.band_cap) {
-        q.band_ids[slot] = make_uint2(ra.tri_id(ia), rb.tri_id(ib));
+        q.band_ids[slot] = ids;
         q.band_d[slot] = d;
       } else {
         S->band_overflow = 1;  // the rescan pass covers every leaf pair
