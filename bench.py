@@ -174,6 +174,9 @@ def run_ours(args):
     # one process per GPU over NCCL; more ranks than visible GPUs (a
     # functional check of the N > 1 path on one device) falls back to gloo
     n_dev = torch.cuda.device_count()
+    if n_dev == 0:
+        # the product path is the CUDA one; there is no CPU fallback to time
+        raise SystemExit("bench.py: no CUDA device visible (the reference arm is --impl reference)")
     backend = "nccl" if world <= n_dev else "gloo"
     local = local % n_dev
     torch.cuda.set_device(local)
