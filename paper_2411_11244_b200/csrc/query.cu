@@ -125,6 +125,20 @@ static void launch_pdl(void (*kernel)(Args...), unsigned grid, unsigned block, c
   GD_CUDA(cudaLaunchKernelEx(&cfg, kernel, q));
 }
 
+// k_refine runs as a resident grid (blocks per SM x SMs) striding over the
+// band: a few hundred blocks for a rings band of ~20K entries instead of
+// thousands of mostly idle ones (each also takes a turn on the done counter)
+template <bool kMax>
+static unsigned refine_grid() {
+  static unsigned g[2] = {0, 0};
+  if (g[kMax] == 0) {
+    int per_sm = 0;
+    GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine<kMax>, kRefineThreads, 0));
+    g[kMax] = (unsigned)(std::max(per_sm, 1) * num_sms());
+  }
+  return g[kMax];
+}
+
 template <bool kMax>
 static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_done) {
   const int sms = num_sms();
@@ -164,12 +178,12 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
     if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
     mark(3);
     k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
-    k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);  // + witness record in its last block
+    k_refine<kMax><<<refine_grid<kMax>(), kRefineThreads, 0, s>>>(q);  // + witness record in its last block
   } else {
     launch_pdl(k_nfilter<kMax, false>, sms * 8, 256, s, q);
     if (!kMax) launch_pdl(k_ntest<kMax>, sms * 4, 256, s, q);
     launch_pdl(k_nfilter<kMax, true>, sms, 256, s, q);
-    launch_pdl(k_refine<kMax>, sms * 16, kRefineThreads, s, q);
+    launch_pdl(k_refine<kMax>, refine_grid<kMax>(), kRefineThreads, s, q);
   }
   mark(4);
   mark(5);
@@ -281,7 +295,7 @@ static void launch_dfs(const QArgs& q, cudaStream_t s) {
   const long long m = q.ma.m;
   if (m > 0) k_dfs<kMax><<<(unsigned)((m + kDfsThreads - 1) / kDfsThreads), kDfsThreads, 0, s>>>(q);
   k_dfs_check<<<1, 1, 0, s>>>(q.S);
-  k_refine<kMax><<<sms * 16, kRefineThreads, 0, s>>>(q);
+  k_refine<kMax><<<refine_grid<kMax>(), kRefineThreads, 0, s>>>(q);
   GD_CUDA(cudaGetLastError());
   count_launches(m > 0 ? 5 : 4);
 }
