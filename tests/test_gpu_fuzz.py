@@ -60,3 +60,26 @@ def test_engine_matches_brute_force(md, gpu, block):
                 d, w = (md.brute_force_min if kind == "min" else md.brute_force_max)(a, b, force=True, dtype=dt)
                 assert r.distance == d, (case, prec, kind, r.distance, d)
                 assert (r.witness.tri_a, r.witness.tri_b) == (w.tri_a, w.tri_b), (case, prec, kind)
+
+
+def test_moved_meshes_and_dfs(md, gpu):
+    """Rigidly moved ring pairs (the lazy device transform against numpy's
+    dgemm vertices of the brute force) and the DFS comparator."""
+    rng = np.random.default_rng(77)
+    for case in range(40):
+        nu, nv = int(rng.integers(8, 40)), int(rng.integers(6, 20))
+        tz, tb = md.ring_pair_base(nu, nv)
+        axis = rng.normal(size=3)
+        xa = md.RigidTransform.from_axis_angle(axis, float(rng.uniform(0, 6.3)), rng.normal(size=3) * 0.3)
+        xb = md.RigidTransform.from_axis_angle(rng.normal(size=3), float(rng.uniform(0, 6.3)), rng.normal(size=3) * 0.3)
+        a, b = md.apply_transform(tz, xa), md.apply_transform(tb, xb)
+        ta, tbt = md.build_f12(tz), md.build_f12(tb)
+        md.refit(ta, a)
+        md.refit(tbt, b)
+        for kind in ("min", "max"):
+            r = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tbt)
+            d, w = (md.brute_force_min if kind == "min" else md.brute_force_max)(a, b, force=True)
+            assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (w.tri_a, w.tri_b), (case, kind)
+            if case % 4 == 0:
+                rd = md.run_dfs_baseline(a, b, tbt, kind)
+                assert rd.distance == d and (rd.witness.tri_a, rd.witness.tri_b) == (w.tri_a, w.tri_b), (case, kind)
