@@ -188,3 +188,19 @@ def test_deformation_frames_and_topology_error(cli, md, gpu, capsys, tmp_path):
     fp.write_text(json.dumps([{"mesh_a": other}]))
     code, out, err = _run(cli, capsys, "query", "--mesh-a", pa, "--mesh-b", pb, "--frames", str(fp))
     assert code == cli.EXIT_INPUT and "TopologyMismatchError" in err
+
+
+@pytest.mark.gpu
+def test_module_entry_point(gpu, tmp_path):
+    """`python -m paper_2411_11244_b200 ...` runs the CLI end to end."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    out = tmp_path / "r.csv"
+    r = subprocess.run([sys.executable, "-m", "paper_2411_11244_b200", "query", "--gen", "interlocked-rings",
+                        "nu=30,nv=15", "--kind", "both", "--format", "csv", "--out", str(out), "--check"],
+                       capture_output=True, text=True, timeout=300, cwd=Path(__file__).resolve().parent.parent)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = list(csv.reader(io.StringIO(out.read_text())))
+    assert len(rows) == 3 and rows[1][1] == "min" and rows[2][1] == "max" and rows[1][-1] == "True"
