@@ -103,6 +103,10 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   const float E = S->slack;
   float upd = 0.f;  // max query only
   unsigned long long tested = 0;
+  Key128 rbest;  // rescan: this thread's best exact key
+  rbest.hi = ~0ull;
+  rbest.lo = ~0ull;
+  const float fb_rescan = kRescan ? __uint_as_float(*reinterpret_cast<volatile unsigned*>(&S->fbest)) : 0.f;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < n; base += stride) {
     const unsigned long long i = base + threadIdx.x;
@@ -147,8 +151,12 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
             if (kMax) upd = fmaxf(upd, d);
             ++tested;
             if (kRescan) {
-              if (kMax ? (d + E >= ub) : (d - E <= ub))
-                atomic_min_key(&S->best, exact_key<kMax>(q, ra.tri_id(ia), rb.tri_id(ib)));
+              // within E of the best float32 distance (k_refine's window), the
+              // thread keeps its best exact key; one atomic per warp below
+              if (kMax ? (d >= fb_rescan - E) : (d <= fb_rescan + E)) {
+                const Key128 k = exact_key<kMax>(q, ra.tri_id(ia), rb.tri_id(ib));
+                if (key_less(k, rbest)) rbest = k;
+              }
             } else {
               // max: appended below, warp-aggregated
               dd[2 * ia + ib] = d;
@@ -224,6 +232,14 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
       commit_bound<kMax>(q, upd);
       atomicMax(&S->fbest, __float_as_uint(upd));
     }
+  }
+  if (kRescan) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const Key128 other = shfl_key(rbest, o);
+      if (key_less(other, rbest)) rbest = other;
+    }
+    if (lane == 0 && rbest.hi != ~0ull) atomic_min_key(&S->best, rbest);
   }
   if (!kRescan) {
     tested = warp_sum_u64(tested);

@@ -35,7 +35,7 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static WsLayout ws_layout(const GdConfig& cfg) {
   WsLayout L;
   L.cap = (unsigned long long)std::max<int64_t>(cfg.front_hard_cap, 4);
-  L.band_cap = cfg.band_cap > 0 ? (unsigned long long)cfg.band_cap : (1ull << 24);  // 200 MB: dense near-contact scenes
+  L.band_cap = cfg.band_cap > 0 ? (unsigned long long)cfg.band_cap : (1ull << 26);  // 800 MB: dense near-contact scenes
   size_t o = 0;
   auto take = [&](size_t& field, size_t bytes) {
     field = o;
