@@ -14,9 +14,11 @@
 //                     on the band entries within E of the best float32
 //                     distance, one thread per entry, lexicographic 128-bit
 //                     key minimum; its last block writes the witness and result
-// The bound is a float32 cell carrying a slack E:
-// culling is conservative, so every pair that can attain the reference's
-// exact answer reaches the exact pass.
+// The kernels after k_traverse use programmatic dependent launch (each waits
+// in griddepcontrol.wait for its predecessor), so their launches overlap the
+// predecessor's drain.  The bound is a float32 cell carrying a slack E
+// (DESIGN.md "Exactness"): culling is conservative, so every pair that can
+// attain the reference's exact answer reaches the exact pass.
 #include <algorithm>
 #include <cstddef>
 #include <cstring>
