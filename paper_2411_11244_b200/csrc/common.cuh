@@ -30,14 +30,19 @@ struct Failure {
     if (!(cond)) throw ::gd::Failure{code, msg}; \
   } while (0)
 
+// per-device launch caches (one host process may drive several GPUs)
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < kMaxDevices ? dev : kMaxDevices - 1;
+}
 inline int num_sms() {
-  static int sms = -1;
-  if (sms < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
-  }
-  return sms;
+  static int sms[kMaxDevices] = {0};
+  const int dev = current_device();
+  if (sms[dev] <= 0 && cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    sms[dev] = 148;
+  return sms[dev];
 }
 
 // ---------------------------------------------------------------------------

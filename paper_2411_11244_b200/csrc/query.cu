@@ -132,13 +132,14 @@ static void launch_pdl(void (*kernel)(Args...), unsigned grid, unsigned block, c
 // thousands of mostly idle ones (each also takes a turn on the done counter)
 template <bool kMax>
 static unsigned refine_grid() {
-  static unsigned g[2] = {0, 0};
-  if (g[kMax] == 0) {
+  static unsigned g[kMaxDevices] = {0};
+  const int dev = current_device();
+  if (g[dev] == 0) {
     int per_sm = 0;
     GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine<kMax>, kRefineThreads, 0));
-    g[kMax] = (unsigned)(std::max(per_sm, 1) * num_sms());
+    g[dev] = (unsigned)(std::max(per_sm, 1) * num_sms());
   }
-  return g[kMax];
+  return g[dev];
 }
 
 template <bool kMax>
@@ -154,19 +155,21 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
   mark(1);
   // persistent traversal: as many blocks as can be co-resident (cooperative
   // launch guarantees it; the grid barrier relies on it)
-  static int grid[2] = {0, 0};
-  if (grid[kMax] == 0) {
+  // (function attributes and occupancy are per device: cached per device)
+  static int grid[kMaxDevices] = {0};
+  const int dev = current_device();
+  if (grid[dev] == 0) {
     GD_CUDA(cudaFuncSetAttribute(k_traverse<kMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kExpandDynSmem));
     int per_sm = 0;
     GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_traverse<kMax>, kExpandThreads,
                                                           kExpandDynSmem));
     GD_CHECK(per_sm >= 1, GD_ERR_CUDA, "k_traverse cannot be resident");
-    grid[kMax] = per_sm * sms;
+    grid[dev] = per_sm * sms;
   }
   {
     void* args[] = {const_cast<QArgs*>(&q)};
-    GD_CUDA(cudaLaunchCooperativeKernel((const void*)k_traverse<kMax>, dim3(grid[kMax]), dim3(kExpandThreads), args,
+    GD_CUDA(cudaLaunchCooperativeKernel((const void*)k_traverse<kMax>, dim3(grid[dev]), dim3(kExpandThreads), args,
                                         kExpandDynSmem, s));
   }
   // the node boxes are read by k_traverse only: a refit for the next frame
