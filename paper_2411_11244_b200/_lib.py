@@ -250,6 +250,16 @@ def device():
     return t.device("cuda", t.cuda.current_device())
 
 
+def check_device(t, what: str):
+    """Device objects (mesh uploads, trees, workspaces) live on the GPU that
+    was current when they were created; using them from another device would
+    hand the kernels foreign pointers."""
+    cur = torch().cuda.current_device()
+    if t.device.index != cur:
+        raise ValueError(f"{what} lives on cuda:{t.device.index} but the current device is cuda:{cur}; "
+                         f"create one per device (one process per GPU)")
+
+
 def stream_ptr():
     return C.c_void_p(torch().cuda.current_stream().cuda_stream)
 

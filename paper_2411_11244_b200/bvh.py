@@ -163,6 +163,7 @@ class F12Bvh:
 
     def device_view(self) -> _lib.GdBvh:
         """C view (include/gdist.h GdBvh), cached until a buffer changes."""
+        _lib.check_device(self._box, "BVH")
         nv = self._vtx32.numel() // 4 if self._mesh is None else self._mesh.n_vertices
         gv = getattr(self, "_gview", None)
         if gv is not None and gv.vtx32 == self._vtx32.data_ptr() and gv.nv == nv:

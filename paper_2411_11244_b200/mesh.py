@@ -166,8 +166,10 @@ class TriangleMesh:
     def device_view(self) -> _lib.GdMesh:
         """C view (include/gdist.h GdMesh); cached -- the mesh is immutable."""
         if self._gview is not None:
+            _lib.check_device(self._root._dev[0], "mesh")
             return self._gview
         vt, tr = self._upload()
+        _lib.check_device(vt, "mesh")
         g = _lib.GdMesh()
         g.vtx = vt.data_ptr()
         g.tri = tr.data_ptr()
