@@ -159,6 +159,19 @@ def config4():
                   "tris_per_mesh": a.n_triangles, "build_s": bs, "query_ms": ms, "e2e_ms": e2e, **result_fields(r)})
         except md.FrontOverflowError as exc:
             emit({"config": 4, "kind": kind, "overflow": str(exc)})
+            # "if it runs, report it at reduced size"
+            for lat, lon in ((201, 200), (301, 300), (501, 500)):
+                ra, rb = md.gen_scene("nested-shells", {"lat": lat, "lon": lon, "r_inner": 0.8, "r_outer": 0.81})
+                rta, rtb, rbs = build_pair(ra, rb)
+                try:
+                    r, ms, e2e = timed_query(ra, rb, rta, rtb, kind, md.EngineConfig(front_hard_cap=1 << 30), reps=3)
+                    emit({"config": 4, "scene": f"nested shells reduced (lat {lat} x lon {lon})", "kind": kind,
+                          "tris_per_mesh": ra.n_triangles, "build_s": rbs, "query_ms": ms, "e2e_ms": e2e,
+                          **result_fields(r)})
+                except md.FrontOverflowError as exc2:
+                    emit({"config": 4, "scene": f"nested shells reduced (lat {lat} x lon {lon})", "kind": kind,
+                          "overflow": str(exc2)})
+                    break
 
 
 def config5():
