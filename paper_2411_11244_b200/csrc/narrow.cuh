@@ -112,12 +112,14 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
     const unsigned long long i = base + threadIdx.x;
     const float ub = load_bound(S), ub2 = ub * ub;
     unsigned mask = 0;
-    uint2 lp = make_uint2(0, 0);
     float dd[4] = {-1.f, -1.f, -1.f, -1.f};  // max: float32 distances of the tested pairs
     unsigned tid[4] = {0u, 0u, 0u, 0u};     // max: their (tri_a, tri_b) halves, packed below
     unsigned tib[4] = {0u, 0u, 0u, 0u};
-    if (i < n && (!culling || survives<kMax>(keys[i], ub2))) {
-      lp = leaves[i];
+    // the entry is loaded with its key, not after the key test: one dependent
+    // round trip less per leaf pair
+    const uint2 lp = i < n ? leaves[i] : make_uint2(0, 0);
+    const float lkey = i < n ? keys[i] : 0.f;
+    if (i < n && (!culling || survives<kMax>(lkey, ub2))) {
       const LeafRec ra = load_leaf(q.A, lp.x), rb = load_leaf(q.B, lp.y);
       const int ca = ra.count(), cb = rb.count();
       Tri<float> ta[2], tb[2];
