@@ -357,8 +357,8 @@ __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : 4) void k_refine(QArgs 
   for (unsigned long long j = (unsigned long long)blockIdx.x * kRefineThreads + threadIdx.x; j < n;
        j += (unsigned long long)gridDim.x * kRefineThreads) {
     const float f = q.band_d[j];
+    const uint2 ids = q.band_ids[j];  // loaded with f: no second dependent round trip
     if (!(kMax ? f >= fb - E : f <= fb + E)) continue;  // +-inf (warm pair) always passes
-    const uint2 ids = q.band_ids[j];
     const Key128 k = exact_key<kMax>(q, ids.x, ids.y);
     if (key_less(k, best)) best = k;
     ++evals;
