@@ -252,3 +252,15 @@ def test_exception_hierarchy(md):
         assert issubclass(cls, md.MeshDistError)
     e = md.FrontOverflowError(10, 2, 4)
     assert (e.candidates, e.front_in, e.cap) == (10, 2, 4)
+
+
+def test_integration_doc_lists_every_entry_point():
+    """INTEGRATION.md maps every C entry point of include/gdist.h to the
+    reference interface it replaces."""
+    import re
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    names = set(re.findall(r"^\w[\w\s\*]*?\b(gd_\w+)\(", (root / "include" / "gdist.h").read_text(), re.M))
+    doc = (root / "INTEGRATION.md").read_text()
+    assert names and not [n for n in sorted(names) if n not in doc]
