@@ -168,7 +168,6 @@ __device__ void init_query(const QArgs& q) {
   S->n_leaf = 0;
   S->n_band = 0;
   S->n_cand = 0;
-  for (int i = 0; i < kMaxIters; ++i) S->t_sweep[i] = 0;
   S->fbest = kMax ? 0u : __float_as_uint(INFINITY);
   S->expanded = 0;
   S->narrow = 0;
@@ -176,8 +175,6 @@ __device__ void init_query(const QArgs& q) {
   S->band_eval = 0;
   S->band_overflow = 0;
   S->ov_cand = S->ov_in = S->ov_cap = 0;
-  for (int i = 0; i <= kMaxIters; ++i) S->cnt[i] = 0;
-  for (int i = 0; i < kMaxIters; ++i) S->culled_it[i] = S->skip_it[i] = 0;
   q.node[0][0] = make_uint2(0, 0);
   q.key[0][0] = key0;
   if (q.A.depth == 0 && q.B.depth == 0) {
@@ -536,6 +533,18 @@ __global__ __launch_bounds__(kExpandThreads, 1024 / kExpandThreads) void k_trave
   volatile QState* V = S;
   const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
   if (rec) init_query<kMax>(q);  // S->bar was zeroed by the host (memset node)
+  if (blockIdx.x == 0) {
+    // per-iteration counters, zeroed by block 0's threads in parallel (the
+    // grid barrier below publishes them)
+    for (int i = threadIdx.x; i <= kMaxIters; i += blockDim.x) {
+      S->cnt[i] = 0;
+      if (i < kMaxIters) {
+        S->culled_it[i] = 0;
+        S->skip_it[i] = 0;
+        S->t_sweep[i] = 0;
+      }
+    }
+  }
   unsigned phase = 0;
   grid_barrier(&S->bar, ++phase);
   unsigned long long n_in = V->n_in;
