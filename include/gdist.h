@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 11
+#define GDIST_ABI_VERSION 12
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -83,10 +83,12 @@ typedef struct GdBvhSizes {
  *              four distinct staged vertices of every leaf (x0 y0 z0 x1 |
  *              y1 z1 x2 y2 | z2 x3 y3 z3; repeats pad leaves with fewer):
  *              the refit streams these instead of gathering vertices
- *   leaf_x   : 2 * ceil(L / 32) + 1 + 2 * (L >> 16) + 4 uint32: per 32
+ *   leaf_x   : 2 * ceil(L / 32) + 1 + 2 * (L >> 16) + 5 uint32: per 32
  *              leaves a mask of the leaves with 5-6 distinct vertices, then
  *              per 32 leaves the rank of their first extra record, then a
- *              counter, then the refit's subtree arrival counters
+ *              counter, then the refit's subtree arrival counters, then the
+ *              float bits of max |coordinate| of the staged vertices (the
+ *              scale of the float32 transform's rounding, read by queries)
  *   leaf_xvtx: 2 * L float4 (capacity): the 5th and 6th distinct vertex
  *              (repeated when only five) of each masked leaf, by rank
  * leaf_vtx, leaf_x and leaf_xvtx are written by gd_stage_vertices; the
@@ -148,6 +150,14 @@ typedef struct GdConfig {
   const void* peer_bounds;
   int32_t n_peers;
   int32_t _pad2;
+  /* front arena capacity in entries (12 bytes each; 0 = 2^26).  Independent
+   * of front_hard_cap, which keeps the reference's FrontOverflowError
+   * semantics on the candidates / survivors of each iteration (summed over
+   * the chunks of an iteration).  A level whose children might not fit the
+   * arena is expanded in chunks, depth first, so
+   * any arena of a few thousand entries completes any query; a larger one
+   * only saves rounds. */
+  int64_t arena_entries;
 } GdConfig;
 
 /* QueryResult (query.py:230-263) + Witness (query.py:136-144). */
@@ -166,6 +176,9 @@ typedef struct GdResult {
   int64_t overflow_cap;
   int32_t iterations;
   int32_t status;
+  int32_t rounds;            /* traversal rounds (one per leaf chunk)          */
+  int32_t pending;           /* nonzero: levels remain -- the caller runs another
+                              * round (gd_query_round); gd_query / collect do */
 } GdResult;
 
 /* IterationStat (query.py:147-162). */
@@ -248,6 +261,12 @@ int gd_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const G
 int gd_query_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                    const GdConfig* cfg, void* workspace, size_t workspace_bytes,
                    GdResult* result_dev, void* stream);
+/* Resume a query whose record (gd_query_collect / gd_query_result_async)
+ * has `pending` set: enqueue traversal round `round` (1, 2, ...: one more
+ * than the record's `rounds`) with its narrow and exact phases on the same
+ * workspace; the record is rewritten at its end.  gd_query loops itself. */
+int gd_query_round(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                   const GdConfig* cfg, void* workspace, size_t workspace_bytes, int round, void* stream);
 /* gd_query_async that also records `traversal_done` (a cudaEvent_t, may be
  * NULL) on `stream` right after the traversal kernel: the node boxes are
  * read by the traversal only, so a refit of these trees for the next frame

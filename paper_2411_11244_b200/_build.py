@@ -28,6 +28,11 @@ NVCC_FLAGS = ARCH + [
 ]
 
 
+# per-source extra flags: the traversal kernel runs 2 blocks x 512 threads per
+# SM (64 registers); its out-of-line sweep functions must fit the same budget
+EXTRA_FLAGS = {"traverse.cu": ["-maxrregcount=64"]}
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
         if cand and Path(cand).exists():
@@ -65,7 +70,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         obj = objdir / (src.name + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *headers, Path(__file__)]):
-            flags = list(NVCC_FLAGS) + [f"-D{d}" for d in defines]
+            flags = list(NVCC_FLAGS) + EXTRA_FLAGS.get(src.name, []) + [f"-D{d}" for d in defines]
             if ptxas_verbose and src.suffix == ".cu":
                 flags += ["-Xptxas", "-v"]
             jobs.append([nvcc, *flags, "-c", str(src), "-o", str(obj)])

@@ -89,6 +89,7 @@ class GdConfig(C.Structure):
         ("peer_bounds", C.c_void_p),
         ("n_peers", C.c_int32),
         ("_pad2", C.c_int32),
+        ("arena_entries", C.c_int64),
     ]
 
 
@@ -108,6 +109,8 @@ class GdResult(C.Structure):
         ("overflow_cap", C.c_int64),
         ("iterations", C.c_int32),
         ("status", C.c_int32),
+        ("rounds", C.c_int32),
+        ("pending", C.c_int32),
     ]
 
 
@@ -146,6 +149,8 @@ _SIGNATURES = {
                            C.c_int, P]),
     "gd_query_async": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
                                  C.POINTER(GdConfig), P, C.c_size_t, P, P]),
+    "gd_query_round": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
+                                 C.POINTER(GdConfig), P, C.c_size_t, C.c_int, P]),
     "gd_query_async_ev": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
                                     C.POINTER(GdConfig), P, C.c_size_t, P, P, P]),
     "gd_query_result_device": (C.c_int, [C.POINTER(GdConfig), P, C.POINTER(C.c_void_p)]),

@@ -157,7 +157,7 @@ class F12Bvh:
         self._vtx32 = _lib.empty(max(nv, 1) * 4, torch.float32)
         self._vmap = _lib.empty(max(nv, 1), torch.int32)
         self._leaf_vtx = _lib.empty(3 * L * 4, torch.float32)
-        self._leaf_x = _lib.torch().zeros(2 * ((L + 31) // 32) + 1 + 2 * (L >> 16) + 4, dtype=torch.int32,
+        self._leaf_x = _lib.torch().zeros(2 * ((L + 31) // 32) + 1 + 2 * (L >> 16) + 5, dtype=torch.int32,
                                           device=_lib.device())
         self._leaf_xvtx = _lib.empty(2 * L * 4, torch.float32)
 

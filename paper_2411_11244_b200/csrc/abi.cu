@@ -28,7 +28,8 @@ void export_boxes(const GdMesh& m, const GdBvh& B, int precision, void* nmin, vo
 void pair_greedy(const double* sa, int64_t n, uint8_t* is_left);
 size_t query_workspace_size(const GdConfig& cfg);
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
-                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done);
+                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done,
+                 int round = 0);
 const void* query_result_device(const GdConfig& cfg, void* ws);
 void* query_bound_device(const GdConfig& cfg, void* ws);
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
@@ -185,6 +186,13 @@ int gd_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const G
     GD_CHECK(mesh_a && mesh_b && a && b && cfg && out, GD_ERR_INVALID, "null argument");
     query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), nullptr);
     query_collect(*cfg, workspace, nullptr, out, stats, max_stats, S(stream));
+    // a front larger than the arena: one more round per leaf chunk
+    for (int r = 1; out->pending && out->status == 0; ++r) {
+      query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), nullptr, r);
+      query_collect(*cfg, workspace, nullptr, out, stats, max_stats, S(stream));
+    }
+    if (out->status == GD_ERR_WORKSPACE)
+      throw Failure{GD_ERR_WORKSPACE, "front arena too small (GdConfig.arena_entries)"};
     if (out->status == GD_ERR_FRONT_OVERFLOW)
       throw Failure{GD_ERR_FRONT_OVERFLOW, "front expansion would create " + std::to_string(out->overflow_candidates) +
                                                " candidate pairs from " + std::to_string(out->overflow_front_in) +
@@ -198,6 +206,15 @@ int gd_query_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, c
   return guarded([&] {
     GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
     query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream), nullptr);
+  });
+}
+
+int gd_query_round(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b, const GdConfig* cfg,
+                   void* workspace, size_t workspace_bytes, int round, void* stream) {
+  return guarded([&] {
+    GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
+    GD_CHECK(round >= 1, GD_ERR_INVALID, "gd_query_round resumes a query: round must be >= 1");
+    query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), nullptr, round);
   });
 }
 

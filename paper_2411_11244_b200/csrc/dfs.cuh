@@ -35,6 +35,7 @@ __global__ void k_dfs_init(QArgs q) {
   float M = __uint_as_float(S->dfs_coord);
 #pragma unroll
   for (int k = 0; k < 3; ++k) M = fmaxf(M, fmaxf(fabsf(rb.lo[k]), fabsf(rb.hi[k])));
+  M = fmaxf(M, 0.125f * xf_mag(q.xb, stage_mag(q.B)));  // B's float32 transform rounding (init_query)
   // a little above the engine's 2^-15: A's float32 triangles here are the
   // float64-transformed ones rounded (mesh_tri), B's the staged ones
   S->slack = M * 0x1p-14f;
@@ -44,7 +45,9 @@ __global__ void k_dfs_init(QArgs q) {
   S->done = 0;
   S->err = 0;
   S->iter = 0;
-  S->leaf_buf = 1;
+  S->n_leaf = 0;
+  S->rounds = 1;
+  S->pending = 0;
   S->n_band = 0;
   S->fbest = kMax ? 0u : __float_as_uint(INFINITY);
   S->expanded = 0;

@@ -44,19 +44,39 @@ inline XfF32 xf32_host(const GdMesh& m) {
   x.has = m.has_xf;
   return x;
 }
+// One level of the traversal's front stack: node pairs at one depth pair,
+// entries [off, off + n) of the front arena, [off, off + cur) already expanded.
+// The arena holds two stacks growing towards each other (end 0 from index 0
+// up, end 1 from the arena's top down); a level's children go to the other
+// end, so a sweep never writes the range it reads, and a level consumed in one
+// sweep frees its space at once (breadth-first fronts ping-pong between the
+// ends like a double buffer).  See DESIGN.md "Front arena".
+struct Level {
+  unsigned long long off, n, cur;
+  int da, db;  // depth pair (query.py:116-133: one per front)
+  int it;      // iteration index (IterationStat) of the sweeps expanding it
+  int end;     // 0 = low stack, 1 = high stack
+};
+constexpr int kMaxLevels = 64;
+
 // Device-resident query state (lives at the start of the workspace).
 struct alignas(16) QState {
   Key128 best;                       // exact (distance, tri_a, tri_b) key
   unsigned int bound_bits;           // float32 bits of the slack-carrying bound
   unsigned int done;                 // last-block-done counter
   int err;
-  int cur;                           // input front buffer (0/1)
-  int depth_a, depth_b;
-  int iter;
-  int leaf_buf;                      // buffer holding the leaf-pair list
-  unsigned long long n_in, n_out, n_leaf, n_band;
+  int iter;                          // iterations (levels) recorded so far
+  int sp;                            // front stack depth
+  int chunked;                       // a level did not fit the arena: k = 1 from then on
+  int pending;                       // a leaf chunk went to the narrow phase, levels remain
+  int rounds;                        // traversal rounds (k_traverse launches) so far
+  unsigned long long lo_top, hi_bot; // arena stack tops (entries); gap = [lo_top, hi_bot)
+  unsigned long long leaf_off, n_leaf;   // this round's leaf-pair list (arena entries)
+  int leaf_end, _pad0;
+  unsigned long long cand_off, cand_cap; // triangle-pair candidates (k_nfilter -> k_ntest), in the gap
+  unsigned long long n_band;
   unsigned long long n_cand;         // triangle-pair candidates (k_nfilter)
-  unsigned long long expanded, narrow, culled, band_eval;
+  unsigned long long expanded, narrow, culled, band_eval, ncand_total;
   long long ov_cand, ov_in, ov_cap;
   float slack;
   int band_overflow;
@@ -64,9 +84,13 @@ struct alignas(16) QState {
   unsigned fbest;                    // best float32 narrow distance (ordered bits)
   unsigned dfs_coord;                // per-triangle DFS: max |coordinate| of A (float bits)
   unsigned long long visited;        // per-triangle DFS: node examinations
-  unsigned long long cnt[kMaxIters + 1];       // iteration i: survivors (low 40 bits) + arrivals
-  unsigned long long culled_it[kMaxIters];     // pairs culled in iteration i
+  unsigned long long cnt[3];                   // sweep i % 3: survivors (low 40 bits) + arrivals
+  unsigned long long culled_it[kMaxIters];     // reference-equivalent candidates culled, per iteration
   unsigned long long skip_it[kMaxIters];       // candidates of pairs another split rank owns
+  unsigned long long tot_cand[kMaxIters];      // candidates expanded per iteration (all chunks)
+  unsigned long long tot_in[kMaxIters];        // front entries expanded per iteration
+  unsigned long long tot_out[kMaxIters];       // survivors per iteration
+  Level lv[kMaxLevels];              // the front stack (persists across rounds)
   GdResult res;                      // the result record, then the stats: one
   GdIterStat stats[kMaxIters];       // contiguous device->host copy
   unsigned long long t_it[kMaxIters + 1];      // %globaltimer at iteration boundaries
@@ -78,14 +102,15 @@ struct QArgs {
   GdMesh ma, mb;
   XfF32 xa, xb;  // float32 transforms of ma, mb (xf32_host)
   int profile;    // record per-iteration sweep times (gd_set_profiling)
+  int round;      // traversal round (0: the query starts)
   GdBvh A, B;
   GdConfig cfg;
   QState* S;
-  uint2* node[2];
-  float* key[2];
+  uint2* fnode;                 // front arena: node pairs ...
+  float* fkey;                  // ... and their squared keys
   uint2* band_ids;
   float* band_d;
-  unsigned long long cap;       // front / leaf-list capacity (entries)
+  unsigned long long arena;     // front arena capacity (entries)
   unsigned long long band_cap;  // band capacity (entries)
   GdResult* result;             // device result record
 };
@@ -207,15 +232,24 @@ __device__ __forceinline__ Tri<T> mesh_tri(const GdMesh& m, long long t) {
   return r;
 }
 
-// adaptive_depth (query.py:266-284)
-__device__ __forceinline__ int adaptive_k(unsigned long long n, long long front_cap, int depth_cap,
-                                          int max_remaining) {
-  int k = 1;
-  while (k < depth_cap && k < max_remaining && (unsigned long long)(n << (2 * (k + 1))) <
-                                                   (unsigned long long)front_cap &&
-         2 * (k + 1) < 64 && (n >> (62 - 2 * (k + 1))) == 0)
-    ++k;
-  return k;
+// leaf_x slot (gdist.h) holding the float bits of max |coordinate| of the
+// staged float32 base vertices (k_stage): the scale of the float32
+// transform's rounding, which the slack must cover
+__host__ __device__ __forceinline__ long long stage_mag_slot(long long leaf_count) {
+  return 2 * ((leaf_count + 31) / 32) + 1 + 2 * (leaf_count >> 16) + 4;
+}
+__device__ __forceinline__ float stage_mag(const GdBvh& T) {
+  return __uint_as_float(*reinterpret_cast<const volatile unsigned*>(T.leaf_x + stage_mag_slot(T.leaf_count)));
+}
+// bound on |x'| for x' = R v + t with |v| <= vmax per coordinate, and on the
+// partial sums of xf_apply's FMA chain
+__device__ __forceinline__ float xf_mag(const XfF32& x, float vmax) {
+  if (!x.has) return vmax;
+  float m = 0.f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    m = fmaxf(m, (fabsf(x.r[3 * i]) + fabsf(x.r[3 * i + 1]) + fabsf(x.r[3 * i + 2])) * vmax + fabsf(x.t[i]));
+  return m;
 }
 
 }  // namespace gd

@@ -93,10 +93,11 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   const unsigned long long n = S->n_leaf;
   if (n == 0) return;
   if (kRescan && *reinterpret_cast<volatile int*>(&S->band_overflow) == 0) return;
-  const int buf = S->leaf_buf;
-  const uint2* leaves = q.node[buf];
-  const float* keys = q.key[buf];
-  uint2* out = q.node[buf ^ 1];
+  // this round's leaf-pair list and the candidate list (the arena's gap)
+  const uint2* leaves = q.fnode + S->leaf_off;
+  const float* keys = q.fkey + S->leaf_off;
+  uint2* out = q.fnode + S->cand_off;
+  const unsigned long long cand_cap = S->cand_cap;
   const bool culling = q.cfg.culling != 0;
   const XfF32 xa = q.xa, xb = q.xb;
   const int lane = threadIdx.x & 31;
@@ -219,7 +220,7 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (mask & (1u << c)) {
-          if (pos < q.cap)
+          if (pos < cand_cap)
             out[pos] = make_uint2(2 * lp.x + (c >> 1), 2 * lp.y + (c & 1));
           else
             S->band_overflow = 1;  // the rescan pass covers every leaf pair
@@ -255,10 +256,10 @@ template <bool kMax>
 __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
-  const unsigned long long n = min(S->n_cand, q.cap);
+  const unsigned long long n = min(S->n_cand, S->cand_cap);
   if (n == 0) return;
   if (blockIdx.x * 256ull >= n) return;
-  const uint2* cand = q.node[S->leaf_buf ^ 1];
+  const uint2* cand = q.fnode + S->cand_off;
   const float E = S->slack;
   const XfF32 xa = q.xa, xb = q.xb;
   __shared__ float warp_upd[8];
@@ -500,6 +501,8 @@ __device__ void finalize(const QArgs& q) {
   r.overflow_candidates = S->ov_cand;
   r.overflow_front_in = S->ov_in;
   r.overflow_cap = S->ov_cap;
+  r.rounds = S->rounds;
+  r.pending = S->pending;
   if (!found) {
     r.tri_a = r.tri_b = -1;
     const float b = load_bound(S);

@@ -28,15 +28,20 @@
 namespace gd {
 
 struct WsLayout {
-  size_t state, node0, key0, node1, key1, band_ids, band_d, result, total;
-  unsigned long long cap, band_cap;
+  size_t state, fnode, fkey, band_ids, band_d, result, total;
+  unsigned long long arena, band_cap;
 };
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// The front arena is sized by the caller (GdConfig.arena_entries; the Python
+// layer derives it from the free HBM), independent of front_hard_cap: a
+// level that does not fit is expanded in chunks (traverse.cuh plan_sweep).
+constexpr unsigned long long kDefaultArena = 1ull << 26;  // 768 MB
 static WsLayout ws_layout(const GdConfig& cfg) {
   WsLayout L;
-  L.cap = (unsigned long long)std::max<int64_t>(cfg.front_hard_cap, 4);
+  L.arena = cfg.arena_entries > 0 ? (unsigned long long)cfg.arena_entries : kDefaultArena;
+  L.arena = std::max<unsigned long long>(L.arena, 64);
   L.band_cap = cfg.band_cap > 0 ? (unsigned long long)cfg.band_cap : (1ull << 26);  // 800 MB: dense near-contact scenes
   size_t o = 0;
   auto take = [&](size_t& field, size_t bytes) {
@@ -45,10 +50,8 @@ static WsLayout ws_layout(const GdConfig& cfg) {
   };
   take(L.state, sizeof(QState));
   take(L.result, sizeof(GdResult));
-  take(L.node0, L.cap * sizeof(uint2));
-  take(L.key0, L.cap * sizeof(float));
-  take(L.node1, L.cap * sizeof(uint2));
-  take(L.key1, L.cap * sizeof(float));
+  take(L.fnode, L.arena * sizeof(uint2));
+  take(L.fkey, L.arena * sizeof(float));
   take(L.band_ids, L.band_cap * sizeof(uint2));
   take(L.band_d, L.band_cap * sizeof(float));
   L.total = o;
@@ -63,6 +66,8 @@ static void validate(const GdBvh& a, const GdBvh& b, const GdConfig& cfg) {
   GD_CHECK(cfg.front_cap >= 4, GD_ERR_CONFIG, "front_cap must be >= 4");
   GD_CHECK(cfg.depth_cap >= 1 && cfg.depth_cap <= 16, GD_ERR_CONFIG, "depth_cap must be in [1, 16]");
   GD_CHECK(cfg.front_hard_cap >= 4, GD_ERR_CONFIG, "front_hard_cap must be >= 4");
+  GD_CHECK(cfg.arena_entries >= 0 && cfg.arena_entries < (1ll << 31), GD_ERR_CONFIG,
+           "arena_entries must be in [0, 2^31)");
   GD_CHECK(cfg.frame == 0 || cfg.frame == 1, GD_ERR_CONFIG, "frame must be 0 (world) or 1 (B-local)");
   GD_CHECK(cfg.n_peers >= 0 && cfg.n_peers <= 64 && (cfg.n_peers == 0 || cfg.peer_bounds), GD_ERR_INVALID,
            "peer_bounds must list n_peers (<= 64) bound cells");
@@ -154,23 +159,24 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
   GD_CUDA(cudaMemsetAsync(&q.S->bar, 0, sizeof(unsigned), s));
   mark(1);
   // persistent traversal: as many blocks as can be co-resident (cooperative
-  // launch guarantees it; the grid barrier relies on it)
+  // launch guarantees it; the grid barrier relies on it); the split-query
+  // variant carries the ownership tests
   // (function attributes and occupancy are per device: cached per device)
-  static int grid[kMaxDevices] = {0};
+  const bool split = q.cfg.split_world > 1;
+  auto kern = kMax ? (split ? k_traverse_max_split : k_traverse_max) : (split ? k_traverse_min_split : k_traverse_min);
+  static int grid[kMaxDevices][2] = {{0}};
   const int dev = current_device();
-  if (grid[dev] == 0) {
-    GD_CUDA(cudaFuncSetAttribute(k_traverse<kMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kExpandDynSmem));
+  int& g = grid[dev][split ? 1 : 0];
+  if (g == 0) {
+    GD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kExpandDynSmem));
     int per_sm = 0;
-    GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_traverse<kMax>, kExpandThreads,
-                                                          kExpandDynSmem));
+    GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kExpandThreads, kExpandDynSmem));
     GD_CHECK(per_sm >= 1, GD_ERR_CUDA, "k_traverse cannot be resident");
-    grid[dev] = per_sm * sms;
+    g = per_sm * sms;
   }
   {
     void* args[] = {const_cast<QArgs*>(&q)};
-    GD_CUDA(cudaLaunchCooperativeKernel((const void*)k_traverse<kMax>, dim3(grid[dev]), dim3(kExpandThreads), args,
-                                        kExpandDynSmem, s));
+    GD_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(g), dim3(kExpandThreads), args, kExpandDynSmem, s));
   }
   // the node boxes are read by k_traverse only: a refit for the next frame
   // may start once this event has fired
@@ -219,22 +225,26 @@ static QArgs make_args(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const
   q.B = b;
   q.cfg = cfg;
   q.S = reinterpret_cast<QState*>(base + L.state);
-  q.node[0] = reinterpret_cast<uint2*>(base + L.node0);
-  q.node[1] = reinterpret_cast<uint2*>(base + L.node1);
-  q.key[0] = reinterpret_cast<float*>(base + L.key0);
-  q.key[1] = reinterpret_cast<float*>(base + L.key1);
+  q.round = 0;
+  q.fnode = reinterpret_cast<uint2*>(base + L.fnode);
+  q.fkey = reinterpret_cast<float*>(base + L.fkey);
   q.band_ids = reinterpret_cast<uint2*>(base + L.band_ids);
   q.band_d = reinterpret_cast<float*>(base + L.band_d);
-  q.cap = L.cap;
+  q.arena = L.arena;
   q.band_cap = L.band_cap;
   q.result = result_dev;  // nullptr: the record stays in the state block (QState::res)
   return q;
 }
 
+// round 0 starts the query; round r > 0 resumes a query whose record says
+// `pending` (its last round ended with a leaf chunk while levels remained)
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
-                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done) {
+                 void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done,
+                 int round) {
   validate(a, b, cfg);
+  GD_CHECK(round >= 0, GD_ERR_INVALID, "round must be >= 0");
   QArgs q = make_args(ma, mb, a, b, cfg, ws, ws_bytes, result_dev);
+  q.round = round;
   if (g_profile) g_last_state = q.S;
   if (cfg.kind == 1)
     launch_query<true>(q, s, traversal_done);

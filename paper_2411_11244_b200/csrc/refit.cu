@@ -23,11 +23,20 @@ constexpr int kFold = 256;  // nodes per block per fold (8 levels)
 // gdist.h sizes the cascade counters in leaf_x for 256-leaf blocks (2 (L >> 16) + 4)
 static_assert(kFold == 256, "leaf_x cascade counter capacity assumes 256-leaf blocks");
 
-__global__ __launch_bounds__(256) void k_stage(GdMesh m, const int32_t* __restrict__ vmap, float4* __restrict__ out) {
+// also records max |coordinate| of the staged vertices (stage_mag_slot, the
+// scale of the float32 transform's rounding; NaN coordinates are ignored)
+__global__ __launch_bounds__(256) void k_stage(GdMesh m, const int32_t* __restrict__ vmap, float4* __restrict__ out,
+                                               unsigned* __restrict__ mag) {
   const long long i = blockIdx.x * 256ll + threadIdx.x;
-  if (i >= m.nv) return;
-  const double* p = m.vtx + 3 * i;
-  out[vmap[i]] = make_float4((float)p[0], (float)p[1], (float)p[2], 0.f);
+  float a = 0.f;
+  if (i < m.nv) {
+    const double* p = m.vtx + 3 * i;
+    const float4 v = make_float4((float)p[0], (float)p[1], (float)p[2], 0.f);
+    out[vmap[i]] = v;
+    a = fmaxf(fabsf(v.x), fmaxf(fabsf(v.y), fabsf(v.z)));
+  }
+  a = warp_max(a);
+  if ((threadIdx.x & 31) == 0 && a > 0.f) atomicMax(mag, __float_as_uint(a));
 }
 
 // union of this lane's box with the one `o` lanes up (mask: the block's lanes
@@ -229,11 +238,13 @@ __global__ __launch_bounds__(256) void k_leaf_vtx(GdBvh T) {
 void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "mesh vertex count differs from the tree's");
   GD_CHECK(T.leaf_vtx && T.leaf_x && T.leaf_xvtx, GD_ERR_INVALID, "GdBvh leaf vertex sets must be allocated");
-  if (m.nv > 0)
-    k_stage<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, T.vmap, reinterpret_cast<float4*>(T.vtx32));
   const long long W = (T.leaf_count + 31) / 32;
-  // extras counter + the refit's cascade counters (gdist.h leaf_x)
-  GD_CUDA(cudaMemsetAsync(T.leaf_x + 2 * W, 0, (1 + 2 * (T.leaf_count >> 16) + 4) * sizeof(uint32_t), s));
+  // extras counter + the refit's cascade counters + the staging magnitude
+  // (gdist.h leaf_x)
+  GD_CUDA(cudaMemsetAsync(T.leaf_x + 2 * W, 0, (1 + 2 * (T.leaf_count >> 16) + 4 + 1) * sizeof(uint32_t), s));
+  if (m.nv > 0)
+    k_stage<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, T.vmap, reinterpret_cast<float4*>(T.vtx32),
+                                                           T.leaf_x + stage_mag_slot(T.leaf_count));
   k_leaf_vtx<<<(unsigned)((T.leaf_count + 255) / 256), 256, 0, s>>>(T);
   GD_CUDA(cudaGetLastError());
 }

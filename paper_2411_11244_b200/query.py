@@ -45,6 +45,9 @@ class EngineConfig:
     guarantee_witness: bool = False
     front_hard_cap: int = 16_777_216
     batch_size: int = 65_536
+    # device extension: front arena entries (12 B each); 0 = sized from the
+    # free HBM.  Independent of front_hard_cap.
+    arena_entries: int = 0
 
     def __post_init__(self):
         if self.front_cap < 4:
@@ -57,6 +60,8 @@ class EngineConfig:
             raise ConfigError(f"batch_size must be >= 4, got {self.batch_size}")
         if self.front_hard_cap < 4:
             raise ConfigError("front_hard_cap must be >= 4")
+        if self.arena_entries < 0:
+            raise ConfigError(f"arena_entries must be >= 0, got {self.arena_entries}")
         if isinstance(self.threads, str):
             if self.threads != "auto":
                 raise ConfigError(f"threads must be a positive int or 'auto', got {self.threads!r}")
@@ -234,22 +239,45 @@ _MAX_STATS = 64
 
 
 class _Workspace:
-    """Per-device scratch for the query engine, grown on demand and reused."""
+    """Query scratch (front arena, band, state), per device AND per host
+    thread -- two threads querying at once never share a workspace -- grown
+    on demand and reused."""
 
-    _cache: dict = {}
-    _lock = threading.Lock()
+    _tls = threading.local()
 
     @classmethod
     def get(cls, nbytes: int):
         torch = _lib.torch()
         dev = torch.cuda.current_device()
-        with cls._lock:
-            t = cls._cache.get(dev)
-            if t is None or t.numel() < nbytes:
-                cls._cache.pop(dev, None)
-                t = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", dev))
-                cls._cache[dev] = t
-            return t
+        cache = getattr(cls._tls, "cache", None)
+        if cache is None:
+            cache = cls._tls.cache = {}
+        t = cache.get(dev)
+        if t is None or t.numel() < nbytes:
+            cache.pop(dev, None)
+            t = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", dev))
+            cache[dev] = t
+        return t
+
+
+_ARENA_MIN, _ARENA_MAX = 1 << 26, 1 << 30
+_arena_auto: dict = {}
+_arena_lock = threading.Lock()
+
+
+def _auto_arena() -> int:
+    """Front arena entries from the free HBM of the current device: an
+    eighth of it, clamped to [2^26, 2^30] entries (0.8 - 12.9 GB), a power of
+    two so repeated plans share one workspace size; decided once per device."""
+    torch = _lib.torch()
+    dev = torch.cuda.current_device()
+    with _arena_lock:
+        n = _arena_auto.get(dev)
+        if n is None:
+            free, _total = torch.cuda.mem_get_info(dev)
+            n = max(_ARENA_MIN, min(_ARENA_MAX, 1 << max(0, (free // 8 // 12).bit_length() - 1)))
+            _arena_auto[dev] = n
+        return n
 
 
 def _gd_config(cfg: EngineConfig, kind: str, warm_pair, band_cap: int = 0) -> _lib.GdConfig:
@@ -268,6 +296,7 @@ def _gd_config(cfg: EngineConfig, kind: str, warm_pair, band_cap: int = 0) -> _l
         g.warm_a = g.warm_b = -1
     g.band_cap = band_cap
     g.split_rank, g.split_world, g.split_level = 0, 1, 11
+    g.arena_entries = cfg.arena_entries or _auto_arena()
     return g
 
 
@@ -345,10 +374,26 @@ class PreparedQuery:
                                                 self.ws.numel(), None, stream or _lib.stream_ptr(), ev), "query")
 
     def collect(self, stream=None) -> QueryResult:
-        _lib.check(_lib.lib().gd_query_collect(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg),
-                                               _lib.ptr(self.ws), None, C.byref(self.res), self.stats, _MAX_STATS,
-                                               stream or _lib.stream_ptr()), "query")
+        s = stream or _lib.stream_ptr()
+        L = _lib.lib()
+        _lib.check(L.gd_query_collect(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg), _lib.ptr(self.ws),
+                                      None, C.byref(self.res), self.stats, _MAX_STATS, s), "query")
+        self._finish_rounds(self.res, s)
         return _result(self.kind, self.res, self.stats)
+
+    def _finish_rounds(self, res, s):
+        """A front larger than the arena is expanded in chunks: every leaf
+        chunk ends a traversal round, and the record says `pending` until the
+        last one (gd_query_round)."""
+        L = _lib.lib()
+        while res.pending and res.status == 0:
+            _lib.check(L.gd_query_round(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a), C.byref(self.g_b),
+                                        C.byref(self.g_cfg), _lib.ptr(self.ws), self.ws.numel(), int(res.rounds), s),
+                       "query_round")
+            _lib.check(L.gd_query_collect(C.byref(self.g_a), C.byref(self.g_b), C.byref(self.g_cfg),
+                                          _lib.ptr(self.ws), None, C.byref(self.res), self.stats, _MAX_STATS, s),
+                       "query")
+            res = self.res
 
     def run(self) -> QueryResult:
         self.launch()
@@ -392,18 +437,25 @@ class PreparedQuery:
         base = self._pinned.data_ptr()
         r = _lib.GdResult.from_address(base)
         stats = (_lib.GdIterStat * _MAX_STATS).from_address(base + C.sizeof(_lib.GdResult))
+        if r.pending and r.status == 0:
+            self._finish_rounds(r, _lib.stream_ptr())
+            return _result(self.kind, self.res, self.stats)
         return _result(self.kind, r, stats)
 
 
-# recently used query plans, keyed by (trees, config, kind, warm pair, device);
-# the trees are held weakly
-_PLANS: "dict" = {}
+# recently used query plans of this host thread (a plan uses the thread's
+# workspace), keyed by (trees, config, kind, warm pair, device); the trees are
+# held weakly
+_PLANS_TLS = threading.local()
 _PLANS_MAX = 16
 
 
 def _plan(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair) -> PreparedQuery:
     import weakref
 
+    _PLANS = getattr(_PLANS_TLS, "plans", None)
+    if _PLANS is None:
+        _PLANS = _PLANS_TLS.plans = {}
     wp = None if warm_pair is None else (int(warm_pair[0]), int(warm_pair[1]))
     key = (id(bvh_a), id(bvh_b), cfg, kind, wp, _lib.torch().cuda.current_device())
     ent = _PLANS.get(key)
@@ -423,6 +475,9 @@ def _plan(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair) -> PreparedQuery:
 def _result(kind: str, r: _lib.GdResult, stats) -> QueryResult:
     if r.status == _lib.GD_ERR_FRONT_OVERFLOW:
         raise _lib.overflow_error(r)
+    if r.status == _lib.GD_ERR_WORKSPACE:
+        raise RuntimeError("front arena too small for this query (EngineConfig.arena_entries); "
+                           "a few entries per tree level are needed")
     if r.status != 0:
         raise RuntimeError(f"device query failed with status {r.status}")
     its = tuple(

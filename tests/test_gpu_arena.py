@@ -1,0 +1,120 @@
+"""Front arena: the traversal's level stack in an
+arena sized independently of front_hard_cap, chunked depth-first expansion
+when a level does not fit, and the reference's iteration statistics and
+FrontOverflowError semantics on top of it."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _scene(md, name):
+    if name == "rings":
+        a, b = md.ring_pair_base(250, 100)  # 50K triangles each
+        xa, xb = md.ring_frame_transforms(11)
+        return md.apply_transform(a, xa), md.apply_transform(b, xb)
+    if name == "shells":
+        return md.gen_scene("nested-shells", {"lat": 40, "lon": 48, "r_inner": 0.8, "r_outer": 0.81})
+    return md.gen_scene(name, {"n": 400, "seed": 3})
+
+
+def _trees(md, a, b):
+    return md.build_f12(a), md.build_f12(b)
+
+
+@pytest.mark.parametrize("kind", ["min", "max"])
+@pytest.mark.parametrize("scene", ["rings", "shells"])
+def test_iteration_stats_follow_reference_schedule(md, gpu, kind, scene):
+    """k of every iteration is the reference's adaptive_depth of its front
+    (query.py:266-284); fronts chain (front_out[i] == front_in[i+1]); every
+    candidate is either culled or survives (the last iteration's survivors
+    are the leaf pairs, not a front: front_out 0); the bound is monotone."""
+    a, b = _scene(md, scene)
+    ta, tb = _trees(md, a, b)
+    cfg = md.EngineConfig(front_hard_cap=1 << 30)
+    r = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb, cfg)
+    its = r.iterations
+    assert its and its[-1].front_out == 0
+    da = db = 0
+    total = 0
+    for i, s in enumerate(its):
+        rem_a, rem_b = ta.depth - da, tb.depth - db
+        assert s.k == md.adaptive_depth(s.front_in, cfg, max(rem_a, rem_b)), (i, s)
+        ka, kb = min(s.k, rem_a), min(s.k, rem_b)
+        cand = s.front_in << (ka + kb)
+        total += cand
+        if i + 1 < len(its):
+            assert s.front_out == its[i + 1].front_in, i
+            assert s.culled + s.front_out == cand, (i, s)
+        else:
+            assert s.culled <= cand
+        da, db = da + ka, db + kb
+        if i:
+            prev = its[i - 1].bound_after
+            assert (s.bound_after <= prev) if kind == "min" else (s.bound_after >= prev), i
+    assert (da, db) == (ta.depth, tb.depth)
+    assert r.expanded_pairs == total
+
+
+@pytest.mark.parametrize("kind", ["min", "max"])
+@pytest.mark.parametrize("scene", ["rings", "shells", "random-blobs"])
+def test_chunked_expansion_identical(md, gpu, kind, scene):
+    """Arenas far too small for the fronts force chunked, depth-first
+    expansion over many rounds (one per leaf chunk): the answer is bitwise
+    the breadth-first one, the expanded candidates are accounted per
+    iteration across chunks."""
+    a, b = _scene(md, scene)
+    ta, tb = _trees(md, a, b)
+    run = md.run_min_query if kind == "min" else md.run_max_query
+    want = run(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30))
+    for arena in (1 << 16, 1 << 13, 1 << 10):
+        cfg = md.EngineConfig(front_hard_cap=1 << 30, arena_entries=arena)
+        pq = md.PreparedQuery(a, b, ta, tb, cfg, kind)
+        got = pq.run()
+        assert got.distance == want.distance, (arena, got.distance, want.distance)
+        assert (got.witness.tri_a, got.witness.tri_b) == (want.witness.tri_a, want.witness.tri_b), arena
+        np.testing.assert_array_equal(got.witness.point_a, want.witness.point_a)
+        if arena == 1 << 10 and scene != "random-blobs":  # the blobs' fronts are tiny
+            assert pq.res.rounds > 1, "the small arena must chunk"
+        # per iteration (depth pair) the chunks' fronts add up
+        assert got.iterations[-1].front_out == 0
+        assert all(s.front_in > 0 for s in got.iterations)
+        # synchronous C entry point loops the rounds itself
+        assert run(a, b, ta, tb, cfg).distance == want.distance
+
+
+def test_front_hard_cap_semantics_independent_of_arena(md, gpu):
+    """FrontOverflowError (query.py:373-376, 448-449) depends on
+    front_hard_cap only: the same query overflows with a roomy arena
+    (breadth first) and with a tiny one (chunked, iteration totals)."""
+    a, b = _scene(md, "rings")
+    ta, tb = _trees(md, a, b)
+    ok = md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30))
+    cand, da, db = [], 0, 0
+    for s in ok.iterations:
+        ka, kb = min(s.k, ta.depth - da), min(s.k, tb.depth - db)
+        cand.append(s.front_in << (ka + kb))
+        da, db = da + ka, db + kb
+    cap = max(cand) // 2
+    for arena in (0, 1 << 13):
+        with pytest.raises(md.FrontOverflowError) as ei:
+            md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=cap, arena_entries=arena))
+        assert ei.value.cap == cap and ei.value.candidates > cap
+    # a cap well above every iteration's candidates passes in both layouts
+    cap_ok = 4 * max(cand)
+    for arena in (0, 1 << 13):
+        r = md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=cap_ok, arena_entries=arena))
+        assert r.distance == ok.distance
+
+
+def test_arena_too_small_fails_loudly(md, gpu):
+    a, b = _scene(md, "rings")
+    ta, tb = _trees(md, a, b)
+    with pytest.raises(RuntimeError, match="arena"):
+        md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30, arena_entries=64))
+
+
+def test_arena_config_validation(md):
+    with pytest.raises(md.ConfigError):
+        md.EngineConfig(arena_entries=-1)
