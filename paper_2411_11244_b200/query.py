@@ -192,6 +192,7 @@ class QueryResult:
     narrow_pairs: int
     visited_nodes: int | None = None
     band_pairs: int = field(default=0, compare=False)
+    rounds: int = field(default=1, compare=False)  # traversal rounds
 
     @property
     def witness_exact(self) -> bool:
@@ -489,7 +490,7 @@ def _result(kind: str, r: _lib.GdResult, stats) -> QueryResult:
         w = Witness(float(r.witness_distance), int(r.tri_a), int(r.tri_b), np.array(r.point_a[:], dtype=np.float64),
                     np.array(r.point_b[:], dtype=np.float64))
     return QueryResult(kind, float(r.distance), w, its, int(r.expanded_pairs), int(r.narrow_pairs),
-                       band_pairs=int(r.band_pairs))
+                       band_pairs=int(r.band_pairs), rounds=max(1, int(r.rounds)))
 
 
 def _run_query(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, warm_pair=None) -> QueryResult:
