@@ -485,23 +485,19 @@ class _Topology:
 
 
 def host_topology(mesh):
-    """build_f12's topology (bvh.py:267-289) on the host: the oracle's Morton
-    order + surface areas, and the exact O(n log n) greedy pairing of
-    libgdist (host C++, gd_pair_greedy; bit-equal to the reference's greedy)."""
-    import ctypes as C
-
+    """build_f12's topology (bvh.py:267-289) on the host, for the reference
+    arm's untimed setup: the oracle's Morton order + surface areas and its
+    O(n log n) C restatement of the greedy pairing (oracle/pairing.c,
+    bit-equal to the reference's greedy, tests/test_oracle_golden.py) -- no
+    product code on this arm."""
     from oracle import meshdist_oracle as oracle
-    from paper_2411_11244_b200 import _lib
 
     V, T = mesh.vertices, mesh.triangles
     _, order = oracle.morton_order(V, T)
     P = V[T]
     n = len(T)
-    sa = np.ascontiguousarray(oracle.pair_surface_areas(order, P.min(axis=1), P.max(axis=1)), dtype=np.float64)
-    is_left = np.zeros(n, dtype=np.uint8)
-    _lib.check(_lib.lib().gd_pair_greedy(sa.ctypes.data_as(C.c_void_p), n, is_left.ctypes.data_as(C.c_void_p)),
-               "pair_greedy")
-    return _Topology(oracle.leaves_from_pairs(order, np.flatnonzero(is_left), n), order)
+    sa = oracle.pair_surface_areas(order, P.min(axis=1), P.max(axis=1))
+    return _Topology(oracle.leaves_from_pairs(order, oracle.greedy_pairs_fast(sa, n), n), order)
 
 
 def cpu_baseline(args, ctx, budget):

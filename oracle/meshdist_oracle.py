@@ -401,6 +401,35 @@ def greedy_pairs(sa, n):
     return sorted(lefts)
 
 
+_PAIRING = None
+
+
+def greedy_pairs_fast(sa, n):
+    """The same pairing as greedy_pairs (bvh.py:122-166) in O(n log n): the C
+    restatement oracle/pairing.c (oracle_pair_greedy; see its header for the
+    equivalence argument), loaded with ctypes.  Built by oracle/build.py
+    (__graft_entry__.build()).  Returns the sorted left indices."""
+    global _PAIRING
+    import ctypes
+    from pathlib import Path
+
+    if _PAIRING is None:
+        lib = Path(__file__).resolve().parent / "liboracle_pairing.so"
+        if not lib.exists():
+            from oracle import build as _b
+
+            _b.build()
+        h = ctypes.CDLL(str(lib))
+        h.oracle_pair_greedy.restype = ctypes.c_int
+        h.oracle_pair_greedy.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        _PAIRING = h
+    sa = np.ascontiguousarray(sa, dtype=np.float64)
+    is_left = np.zeros(n, dtype=np.uint8)
+    if _PAIRING.oracle_pair_greedy(sa.ctypes.data_as(ctypes.c_void_p), n, is_left.ctypes.data_as(ctypes.c_void_p)):
+        raise MemoryError("oracle_pair_greedy: out of memory")
+    return np.flatnonzero(is_left)
+
+
 def leaves_from_pairs(order, lefts, n):
     """Assemble (L, 2) leaf triangle ids, -1 for singles (bvh.py:168-181)."""
     L = 1 << (n.bit_length() - 1)

@@ -4,10 +4,12 @@
 read-only arrays, same validation errors) and adds a device view: the base
 vertices are uploaded once and cached on the object.  `apply_transform` is
 lazy on the device: the moved mesh shares the base upload and carries the
-composed rigid transform, which the refit and exact kernels apply on the fly
-(no per-frame vertex upload).  Reading `.vertices` of a moved mesh
-materialises it on the host with the reference's own formula
-(`V @ R.T + t`, applied transform by transform), bit for bit.
+rigid transform, which the refit and exact kernels apply on the fly (no
+per-frame vertex upload), in numpy dgemm's arithmetic (bit for bit the
+reference's `V @ R.T + t`).  A transform of an already-moved mesh
+materialises that mesh with the reference formula first (the reference
+applies transforms one by one; a composed transform could differ by an ulp).
+Reading `.vertices` of a moved mesh materialises it on the host the same way.
 """
 
 from __future__ import annotations
@@ -54,15 +56,33 @@ class TriangleMesh:
     def __init__(self, vertices, triangles):
         self._vertices, self._triangles = _validated(vertices, triangles)
         self._root = self
-        self._chain = ()          # host transforms still to apply to root.vertices
-        self._rot = None          # composed device transform (None = identity)
+        self._chain = ()          # host transform still to apply to root.vertices (at most one)
+        self._rot = None          # device transform (None = identity)
         self._trans = None
         self._dev = None
         self._gview = None
 
     # -- lazily moved mesh (apply_transform) ------------------------------
     @classmethod
+    def _trusted(cls, vertices: np.ndarray, triangles: np.ndarray) -> "TriangleMesh":
+        """A mesh over already-validated read-only arrays (no O(m) checks)."""
+        out = cls.__new__(cls)
+        out._vertices, out._triangles = vertices, triangles
+        out._root = out
+        out._chain = ()
+        out._rot = out._trans = None
+        out._dev = out._gview = None
+        return out
+
+    @classmethod
     def _moved(cls, src: "TriangleMesh", xf: "RigidTransform") -> "TriangleMesh":
+        if src._chain:
+            # a transform of an already-moved mesh: the reference applies the
+            # transforms one by one (mesh.py:104), and one composed (R, t) on
+            # the device can differ from that by an ulp -- so the moved mesh's
+            # vertices are materialised with the reference formula and become
+            # the new base (one upload), keeping the device bit-exact
+            src = cls._trusted(src.vertices, src._triangles)
         out = cls.__new__(cls)
         out._vertices = None
         out._triangles = src._triangles

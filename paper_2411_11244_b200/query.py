@@ -261,14 +261,14 @@ class _Workspace:
         return t
 
 
-_ARENA_MIN, _ARENA_MAX = 1 << 26, 1 << 30
+_ARENA_MIN, _ARENA_MAX = 1 << 26, 1 << 28
 _arena_auto: dict = {}
 _arena_lock = threading.Lock()
 
 
 def _auto_arena() -> int:
     """Front arena entries from the free HBM of the current device: an
-    eighth of it, clamped to [2^26, 2^30] entries (0.8 - 12.9 GB), a power of
+    eighth of it, clamped to [2^26, 2^28] entries (0.8 - 3.2 GB), a power of
     two so repeated plans share one workspace size; decided once per device."""
     torch = _lib.torch()
     dev = torch.cuda.current_device()

@@ -1,6 +1,8 @@
 """The oracle restatement reproduces the reference's own outputs (golden
 vectors from tests/golden/make_golden.py) bit for bit.  CPU only."""
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -121,3 +123,54 @@ def test_kat(golden_meta, oracle):
     assert oracle.adaptive_k(1, cfg, 10) == k["adaptive_1"] == 5
     assert oracle.adaptive_k(100000, cfg, 10) == k["adaptive_100000"] == 1
     assert oracle.adaptive_k(1000, cfg, 2) == k["adaptive_1000_rem2"] == 2
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fast_pairing_matches_literal_greedy(oracle, seed):
+    """oracle/pairing.c (the O(n log n) restatement) == the reference's
+    literal greedy loop (bvh.py:122-166) on random and tie-heavy keys."""
+    rng = np.random.default_rng(100 + seed)
+    for n in list(range(2, 80)) + [127, 255, 257, 511, 513, 1023, 2049, 3001]:
+        sa = np.round(rng.random(n - 1) * 8) / 8 if seed % 2 else rng.random(n - 1)
+        assert oracle.greedy_pairs_fast(sa, n).tolist() == oracle.greedy_pairs(sa, n), (seed, n)
+
+
+def test_fast_pairing_large_tori_golden(oracle):
+    """The reference's own pairing of 60K / 120K-triangle tori
+    (tests/golden/golden_r2.npz, make_golden_r2.py)."""
+    import json
+
+    from paper_2411_11244_b200.scenes import ring_pair_base
+
+    here = Path(__file__).resolve().parent / "golden"
+    meta = json.loads((here / "golden_r2.json").read_text())
+    arr = np.load(here / "golden_r2.npz")
+    for rec in meta["pairings"]:
+        tz, _ = ring_pair_base(rec["nu"], rec["nv"])
+        V, T = tz.vertices, tz.triangles
+        _, order = oracle.morton_order(V, T)
+        P = V[T]
+        sa = oracle.pair_surface_areas(order, P.min(axis=1), P.max(axis=1))
+        leaf = oracle.leaves_from_pairs(order, oracle.greedy_pairs_fast(sa, len(T)), len(T))
+        _eq(leaf.astype(np.int32), arr[f"pair_{rec['name']}_leaf"])
+        _eq(order.astype(np.int32), arr[f"pair_{rec['name']}_order"])
+
+
+def test_oracle_nested_shells_config4_geometry(oracle, md):
+    """The oracle's engine reproduces the reference's config-4 geometry
+    answers (nested shells r 0.8 / 0.81, golden_r2.json) at the smallest
+    recorded size: distance and witness, float64 and float32."""
+    import json
+
+    meta = json.loads((Path(__file__).resolve().parent / "golden" / "golden_r2.json").read_text())
+    rec = meta["shells"][0]
+    a, b = md.gen_scene("nested-shells", rec["params"])
+    for prec, dt in ((64, np.float64), (32, np.float32)):
+        ta = oracle.build_tree(a.vertices, a.triangles, dtype=dt)
+        tb = oracle.build_tree(b.vertices, b.triangles, dtype=dt)
+        cfg = oracle.Config(precision=prec, front_hard_cap=1 << 30)
+        for kind in ("min", "max"):
+            r = oracle.run_query(ta, tb, a.triangle_points(dt), b.triangle_points(dt), kind, cfg)
+            want = rec[f"{kind}{prec}"]
+            assert r.distance == want["distance"], (prec, kind)
+            assert (r.tri_a, r.tri_b) == (want["tri_a"], want["tri_b"]), (prec, kind)
