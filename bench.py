@@ -16,6 +16,14 @@ the unmodified reference package (pure Python + numpy) installed into
 baseline/_ref (git-ignored, shipped by gpurun), driven through its public API
 on the same frames with all host threads, bounded steps; the oracle port
 (oracle/, a numpy restatement) stands in only if baseline/_ref is absent.
+
+`--gpus N` without a torchrun environment (WORLD_SIZE unset) launches the N
+ranks itself (torch.distributed.run, one process per GPU, 127.0.0.1); under
+torchrun it never re-launches.  Extra keys of the line: the max query of the
+same frames (`max_query_ms`, its own roofline), refit + min + max per frame
+(config 3), and for N > 1 the single query split over the N ranks
+(`split`, max over ranks).  `--dry-run` exercises the launcher, the process
+group, the max-over-ranks reduction and the result all-gather without a GPU.
 """
 
 from __future__ import annotations
@@ -50,7 +58,60 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=150.0, help="seconds for CPU legs")
     ap.add_argument("--profile-only", action="store_true", help="a short run for ncu (no baselines)")
+    ap.add_argument("--no-max", action="store_true", help="skip the max-query keys")
+    ap.add_argument("--dry-run", action="store_true", help="launcher / collective plumbing only (no GPU work)")
     return ap.parse_args()
+
+
+def self_launch(args) -> int:
+    """`--gpus N` outside torchrun: start the N ranks (one process per GPU)
+    with torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd, cwd=str(REPO)).returncode
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_dry(args):
+    """The N > 1 plumbing without GPU work: process group (NCCL when every
+    rank has a GPU, else gloo), barrier, a max-over-ranks reduction of a
+    per-rank "time" and the frame-result all-gather of parallel.run_frames;
+    rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_11244_b200 import parallel
+
+    world, rank, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([1.0 + rank], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    n_frames = 4 * world + 1
+    res = parallel.run_frames(n_frames, lambda f: (float(f) * 0.5, f, 2 * f))
+    ok = bool(np.all(res[:, 0] == np.arange(n_frames) * 0.5) and np.all(res[:, 2] == 2 * np.arange(n_frames)))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "max_over_ranks": float(t.item()),
+                          "frames_gathered": n_frames, "gather_ok": ok}))
+    if world > 1:
+        dist.destroy_process_group()
+    return ok
 
 
 def workload_name(args):
@@ -153,6 +214,137 @@ def query_bytes(res, depth_a, depth_b):
     total = expand + narrow
     return {"expand_bytes": expand, "narrow_bytes": narrow, "total_bytes": total, "leaf_pairs": leaf_pairs,
             "narrow_flops": res.narrow_pairs * (2100 if res.kind == "min" else 72)}
+
+
+def traverse_roofline(res, phases, bvh_a, bvh_b, kind):
+    """Roofline of k_traverse (the dominant kernel): SURVEY 8(d) algorithmic
+    bytes of this query / its CUDA-event time, against the measured HBM peak;
+    traffic = ncu DRAM bytes of one launch (profiles/kernel_traffic.json)."""
+    qb = query_bytes(res, bvh_a.depth, bvh_b.depth)
+    hbm, _, src = peaks()
+    expand_ms = phases["expand"]
+    achieved = qb["expand_bytes"] / (expand_ms * 1e-3) / 1e9 if expand_ms > 0 else None
+    traffic = None
+    tf = REPO / "profiles" / "kernel_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text())["per_launch_dram_bytes"].get(
+            "k_traverse" if kind == "min" else "k_traverse_max")
+    return {"bound": "hbm", "kernel": f"k_traverse_{kind} (all expansion iterations of one query, one launch)",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
+            "traffic": traffic, "peak_source": src, "algorithmic_bytes": qb["expand_bytes"], "kernel_ms": expand_ms,
+            "note": "algorithmic bytes (SURVEY 8d) count every box load; most hit L2 (traffic = ncu DRAM bytes "
+                    "of one launch, profiles/kernel_traffic.json)"}
+
+
+def max_section(md, _lib, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_dev):
+    """The max query of the same frames: its own time and roofline, and the
+    whole config-3 frame (refit A + refit B + min + max) back to back on the
+    device (CUDA events on the launching stream, max over ranks)."""
+    import ctypes as C
+
+    import torch
+
+    plans = [md.PreparedQuery(a, b, bvh_a, bvh_b, cfg, "max") for a, b, _ in prepared]
+    for i in range(W):
+        a, b, pq = prepared[i]
+        bvh_a._device_refit(a)
+        bvh_b._device_refit(b)
+        plans[i].launch()
+        plans[i].collect()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    if dist:
+        dist.barrier()
+    for j, i in enumerate(range(W, W + K)):
+        a, b, pq = prepared[i]
+        ev[j][0].record(stream)
+        bvh_a._device_refit(a)
+        bvh_b._device_refit(b)
+        ev[j][1].record(stream)
+        pq.launch()
+        ev[j][2].record(stream)
+        plans[i].launch()
+        ev[j][3].record(stream)
+    torch.cuda.synchronize()
+    max_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
+    frame_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in ev]))
+    if dist:
+        t = torch.tensor([max_ms, frame_ms], device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_ms, frame_ms = float(t[0].item()), float(t[1].item())
+    # answers and the profiled phases of the last frame's max query
+    L = _lib.lib()
+    a, b, _ = prepared[-1]
+    bvh_a._device_refit(a)
+    bvh_b._device_refit(b)
+    L.gd_set_profiling(1)
+    plans[-1].launch()
+    res = plans[-1].collect()
+    ph = (C.c_float * 5)()
+    L.gd_query_phase_ms(ph, 5)
+    L.gd_set_profiling(0)
+    phases = {"init": ph[0], "expand": ph[1], "narrow": ph[2], "exact": ph[3], "final": ph[4]}
+    return {"max_query_ms": round(max_ms, 6), "max_phases_ms": {k: round(v, 6) for k, v in phases.items()},
+            "max_distance": res.distance, "max_witness": [res.witness.tri_a, res.witness.tri_b],
+            "max_roofline": traverse_roofline(res, phases, bvh_a, bvh_b, "max"),
+            "frame_min_max_ms": round(frame_ms, 6),
+            "frame_min_max_note": "config 3 per frame: refit A + refit B + min + max, back to back on one stream"}, res
+
+
+def split_section(md, tz, tb, bvh_a, bvh_b, cfg, kind, dist, red_dev, backend, frame=7, reps=5):
+    """One query (frame `frame`, every rank the same) split over the N ranks
+    (parallel.run_split_query): ownership by ancestor-pair hash, exact parts
+    combined in one all-gather; with and without the in-kernel bound
+    exchange.  Time = max over ranks of the mean wall time per collective
+    query (the all-gather's synchronisation included), beside the same query
+    on one GPU (rank 0's plain query)."""
+    import torch
+
+    from paper_2411_11244_b200 import parallel
+
+    xa, xb = md.ring_frame_transforms(frame)
+    a, b = md.apply_transform(tz, xa), md.apply_transform(tb, xb)
+    md.refit(bvh_a, a)
+    md.refit(bvh_b, b)
+    run = md.run_min_query if kind == "min" else md.run_max_query
+    single = run(a, b, bvh_a, bvh_b, cfg)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        s.record()
+        run(a, b, bvh_a, bvh_b, cfg)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    out = {"frame": frame, "single_gpu_query_ms": round(float(np.median(ts)), 6), "modes": {}}
+    modes = [("rank-local bound", False), ("bound shared over CUDA IPC (peer atomics)", True)]
+    for name, share in modes:
+        try:
+            for _ in range(2):
+                r = parallel.run_split_query(a, b, bvh_a, bvh_b, kind, cfg, share_bound=share)
+            assert r.distance == single.distance, (r.distance, single.distance)
+            times = []
+            for _ in range(reps):
+                dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                r = parallel.run_split_query(a, b, bvh_a, bvh_b, kind, cfg, share_bound=share)
+                times.append((time.perf_counter() - t0) * 1e3)
+            mine = torch.tensor([float(np.median(times)), float(r.expanded_pairs)], device=red_dev)
+            allv = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
+            dist.all_gather(allv, mine)
+            ms = max(float(v[0]) for v in allv)
+            work = [float(v[1]) for v in allv]
+            out["modes"][name] = {"ms": round(ms, 6), "expanded_pairs_per_rank": work,
+                                  "busiest_rank_share_of_single": round(max(work) / max(1, single.expanded_pairs), 4),
+                                  "distance_equal_to_single_gpu": bool(r.distance == single.distance)}
+        except Exception as exc:  # report, never hide
+            out["modes"][name] = {"error": repr(exc)}
+    parallel.release_split_plans()
+    out["note"] = ("the traversal's top levels (above the split level) are replicated on every rank; they are "
+                   "latency bound (fronts < 25K entries), so the split pays only on large queries")
+    out["backend"] = backend
+    return {"split": out}
 
 
 def peaks():
@@ -309,20 +501,16 @@ def run_ours(args):
     L.gd_query_phase_ms(ph, 5)
     L.gd_set_profiling(0)
     phases = {"init": ph[0], "expand": ph[1], "narrow": ph[2], "exact": ph[3], "final": ph[4]}
-    qb = query_bytes(res, bvh_a.depth, bvh_b.depth)
-    hbm, sm_max, src = peaks()
-    expand_ms = phases["expand"]
-    achieved = qb["expand_bytes"] / (expand_ms * 1e-3) / 1e9 if expand_ms > 0 else None
-    traffic = None
-    tf = REPO / "profiles" / "kernel_traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text())["per_launch_dram_bytes"].get("k_traverse")
-    roofline = {"bound": "hbm", "kernel": "k_traverse (all expansion iterations of one query, one launch)",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
-                "traffic": traffic, "peak_source": src, "algorithmic_bytes": qb["expand_bytes"],
-                "kernel_ms": expand_ms,
-                "note": "algorithmic bytes (SURVEY 8d) count every box load; most hit L2 (traffic = ncu DRAM "
-                        "bytes of one launch, profiles/kernel_traffic.json)"}
+    roofline = traverse_roofline(res, phases, bvh_a, bvh_b, args.kind)
+
+    # the max query of the same frames (config 3 is min + max per frame)
+    max_keys, max_res = {}, None
+    if not args.no_max and args.kind == "min" and not args.profile_only:
+        max_keys, max_res = max_section(md, _lib, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_dev)
+    # one query split over the N ranks, max over ranks
+    split_keys = {}
+    if N > 1 and not args.profile_only:
+        split_keys = split_section(md, tz, tb, bvh_a, bvh_b, cfg, args.kind, dist, red_dev, backend)
 
     # e2e through the public API: run_sequence over this job's frames (host
     # transforms in, every frame's (distance, tri_a, tri_b) back on the host;
@@ -393,10 +581,12 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clocks,
             "setup_s": round(setup_s, 2),
+            **max_keys,
+            **split_keys,
         }
     if dist:
         dist.barrier()
-    return out, (tz, tb, bvh_a, bvh_b, frames[W:], results)
+    return out, (tz, tb, bvh_a, bvh_b, frames[W:], results, max_res)
 
 
 # ---------------------------------------------------------------------------
@@ -456,7 +646,9 @@ class CpuLeg:
             return f"unmodified reference package (baseline/_ref, numpy, EngineConfig(threads={self.workers}))"
         return f"oracle port of the reference (oracle/, numpy, {self.workers} threads)"
 
-    def frame(self, f):
+    def frame(self, f, kind=None):
+        """(distance, tri_a, tri_b) of frame f's query (default: the leg's kind)."""
+        kind = kind or self.kind
         xa, xb = self.md.ring_frame_transforms(f % 1000)
         if self.ref is not None:
             R = self.ref
@@ -464,8 +656,10 @@ class CpuLeg:
             b = R.apply_transform(self.B0, R.RigidTransform(xb.rotation, xb.translation))
             R.refit(self.ta, a)
             R.refit(self.tb, b)
-            run = R.run_min_query if self.kind == "min" else R.run_max_query
-            return run(a, b, self.ta, self.tb, self.cfg).distance
+            run = R.run_min_query if kind == "min" else R.run_max_query
+            r = run(a, b, self.ta, self.tb, self.cfg)
+            self.last = (a, b)
+            return r.distance, r.witness.tri_a, r.witness.tri_b
         o = self.oracle
         va = o.transform_vertices(self.tz.vertices, xa.rotation, xa.translation)
         vb = o.transform_vertices(self.tbm.vertices, xb.rotation, xb.translation)
@@ -473,8 +667,22 @@ class CpuLeg:
         o.fill_boxes(self.tb, vb, self.tbm.triangles)
         pa = o.triangle_points(va, self.tz.triangles)
         pb = o.triangle_points(vb, self.tbm.triangles)
-        return o.run_query(self.ta, self.tb, pa, pb, self.kind,
-                           o.Config(workers=self.workers, front_hard_cap=1 << 27)).distance
+        r = o.run_query(self.ta, self.tb, pa, pb, kind, o.Config(workers=self.workers, front_hard_cap=1 << 27))
+        self.last = (pa, pb)
+        return r.distance, r.tri_a, r.tri_b
+
+    def pair_distance(self, kind, ta, tb):
+        """The reference's own arithmetic on one triangle pair of the last
+        frame (bounds.py batch_tri_tri_*): classifies a witness tie."""
+        if self.ref is not None:
+            from meshdist import bounds as rb
+
+            a, b = self.last
+            pa, pb = a.triangle_points()[[ta]], b.triangle_points()[[tb]]
+            return float((rb.batch_tri_tri_min if kind == "min" else rb.batch_tri_tri_max)(pa, pb)[0][0])
+        pa, pb = self.last
+        return float((self.oracle.tri_tri_min if kind == "min" else self.oracle.tri_tri_max)(
+            pa[[ta]], pb[[tb]])[0][0])
 
 
 class _Topology:
@@ -501,18 +709,57 @@ def host_topology(mesh):
 
 
 def cpu_baseline(args, ctx, budget):
+    """The reference on the box's host cores, same frame as the GPU's last
+    timed step (SURVEY.md 8(d) protocol, bounded): threads = all cores, best
+    of up to 3 (one warm-up excluded when the budget allows), and threads = 1
+    once; the GPU's answer checked against it -- distance, witness (equal, or
+    a documented tie: the reference arithmetic on the GPU's pair gives the
+    same distance) -- and the max query of the same frame likewise."""
     import paper_2411_11244_b200 as md
 
-    tz, tbm, bvh_a, bvh_b, frames, results = ctx
+    tz, tbm, bvh_a, bvh_b, frames, results, max_res = ctx
+    f = frames[-1]
     workers = os.cpu_count() or 1
     leg = CpuLeg(md, tz, tbm, bvh_a, bvh_b, args.kind, workers)
-    t0 = time.perf_counter()
-    d = leg.frame(frames[-1])
-    sec = time.perf_counter() - t0
-    return {"value": round(sec * 1e3, 3), "unit": "ms/query", "cores": workers, "kind": leg.kind_label,
-            "sample": f"1 frame (f={frames[-1]}) of the same workload: refit A+B + {args.kind} query, "
-                      f"{leg.describe()}",
-            "distance_equal_to_gpu": bool(d == results[-1].distance)}
+    t_start = time.perf_counter()
+    times, out = [], None
+    while len(times) < 3:
+        t0 = time.perf_counter()
+        out = leg.frame(f)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget / 3:
+            break
+    gpu = results[-1]
+
+    def classify(kind, ref, g):
+        d, ta, tb = ref
+        if (g.witness.tri_a, g.witness.tri_b) == (ta, tb):
+            return "equal"
+        same = leg.pair_distance(kind, g.witness.tri_a, g.witness.tri_b) == d
+        return "tie (reference arithmetic on the GPU pair gives the same distance)" if same else "MISMATCH"
+
+    rec = {"value": round(min(times) * 1e3, 3), "unit": "ms/query", "cores": workers, "kind": leg.kind_label,
+           "sample": f"frame f={f} of the same workload: refit A+B + {args.kind} query, {leg.describe()}; "
+                     f"best of {len(times)}",
+           "runs_ms": [round(t * 1e3, 1) for t in times], "cpu_model": cpu_model(), "nproc": workers,
+           "distance_equal_to_gpu": bool(out[0] == gpu.distance),
+           "witness": classify(args.kind, out, gpu), "witness_ref": [out[1], out[2]],
+           "witness_gpu": [gpu.witness.tri_a, gpu.witness.tri_b]}
+    # one thread (the reference's default EngineConfig(threads=1), query.py:57-58)
+    if time.perf_counter() - t_start < budget:
+        leg1 = CpuLeg(md, tz, tbm, bvh_a, bvh_b, args.kind, 1)
+        t0 = time.perf_counter()
+        o1 = leg1.frame(f)
+        rec["threads_1_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+        rec["threads_1_distance_equal"] = bool(o1[0] == out[0])
+    # the max query of the same frame, full scale
+    if max_res is not None and time.perf_counter() - t_start < 2 * budget:
+        t0 = time.perf_counter()
+        om = leg.frame(f, "max")
+        rec["max_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+        rec["max_distance_equal_to_gpu"] = bool(om[0] == max_res.distance)
+        rec["max_witness"] = classify("max", om, max_res)
+    return rec
 
 
 def run_reference(args):
@@ -542,6 +789,12 @@ def run_reference(args):
         if time.perf_counter() - t_start > args.cpu_budget and times:
             break
     value = float(np.mean(times)) * 1e3
+    extra = {}
+    if args.kind == "min" and not args.no_max and time.perf_counter() - t_start < 1.5 * args.cpu_budget:
+        # the max query of one frame (config 3 is min + max per frame)
+        t0 = time.perf_counter()
+        leg.frame(0, "max")
+        extra["max_ms_per_query"] = round((time.perf_counter() - t0) * 1e3, 3)
     return {
         "impl": "reference",
         "metric": METRIC,
@@ -561,13 +814,20 @@ def run_reference(args):
                    "nu": args.nu, "nv": args.nv, "kind": args.kind, "precision": 64},
         "cpu_baseline": {"value": round(value, 3), "unit": "ms/query", "cores": workers, "kind": leg.kind_label,
                          "sample": f"{len(times)} frame steps (bounded to {args.cpu_budget:.0f} s) of the same "
-                                   f"workload, {leg.describe()}"},
+                                   f"workload, {leg.describe()}", "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 3), "unit": "ms/query", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "topology": "tree topology from the oracle's C restatement of the reference's greedy pairing "
+                    "(oracle/pairing.c; the reference's own O(n^2) pairing cannot build 7.5M triangles), untimed",
+        **extra,
     }
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    if args.dry_run:
+        sys.exit(0 if run_dry(args) else 1)
     if args.impl == "reference":
         out = run_reference(args)
         if out is not None:

@@ -39,3 +39,16 @@ def test_gpu_arm_fails_loudly_without_gpu():
         pytest.skip("a GPU is visible")
     r = _run("--steps", "1", "--warmup", "3", "--nu", "40", "--nv", "20", timeout=120)
     assert r.returncode != 0 and "no CUDA device" in r.stderr
+
+
+def test_self_launch_two_ranks_dry_run():
+    """`bench.py --gpus 2` outside torchrun starts the 2 ranks itself
+    (torch.distributed.run on 127.0.0.1, gloo without GPUs): one line from
+    rank 0 with n_gpus 2, the max-over-ranks reduction and the frame
+    all-gather done."""
+    r = _run("--gpus", "2", "--dry-run", timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["dry_run"] and line["gather_ok"] and line["max_over_ranks"] == 2.0
