@@ -149,7 +149,14 @@ typedef struct GdConfig {
    * culls with the best bound found anywhere.  0 / NULL = rank-local. */
   const void* peer_bounds;
   int32_t n_peers;
-  int32_t _pad2;
+  /* expansion schedule: -1 = the reference's adaptive_depth exactly
+   * (query.py:266-284; IterationStat.k follows it); 0 = the device schedule
+   * with its default threshold; > 0 = the device schedule with this
+   * threshold -- fronts of at most that many entries with >= 2 levels left
+   * on both trees expand two levels per iteration (k = 2) in ONE sweep that
+   * culls child pairs before their grandchildren, where the reference rule
+   * would pick k = 1.  Same survivors and answers; fewer grid barriers. */
+  int32_t schedule;
   /* front arena capacity in entries (12 bytes each; 0 = 2^26).  Independent
    * of front_hard_cap, which keeps the reference's FrontOverflowError
    * semantics on the candidates / survivors of each iteration (summed over

@@ -88,7 +88,7 @@ class GdConfig(C.Structure):
         ("warm_from", C.c_void_p),
         ("peer_bounds", C.c_void_p),
         ("n_peers", C.c_int32),
-        ("_pad2", C.c_int32),
+        ("schedule", C.c_int32),
         ("arena_entries", C.c_int64),
     ]
 

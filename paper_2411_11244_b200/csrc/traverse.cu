@@ -445,6 +445,132 @@ __device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* w
   return off + x - v;
 }
 
+// k == 2 sweep (two levels per iteration on both trees): one thread per
+// CHILD pair of a front entry -- the k = 1 expansion of that child pair,
+// without writing the intermediate front.  Thread v handles entry v / 4,
+// child pair v % 4 = (i, j); its loads (the entry, then the children of A
+// child i and of B child j: 3 float4 each) are independent, so one round
+// trip covers both levels.  A child's box is the union of its two
+// children's (the refit's fold: bitwise), so it is not loaded.  Same
+// survivors as the reference's 16-candidate expansion (a grandchild pair's
+// key is monotone in its child pair's); culled counts are the
+// reference-equivalent ones.  Tiles, staging and the bound reduction as in
+// k1_sweep.
+template <bool kMax, bool kSplit>
+__device__ __forceinline__ void k2_sweep(const QArgs& q, ExpandShared& sh, unsigned char* stage, const SweepPlan& p,
+                                         unsigned long long* n_out, int la, int lb) {
+  QState* S = q.S;
+  const unsigned n_v = 4u * (unsigned)p.c;  // child pairs (k2 chunks are < 2^28 entries: rem <= schedule < 2^31 / 16)
+  const uint2* __restrict__ in_node = q.fnode + p.in_off;
+  const float* __restrict__ in_key = q.fkey + p.in_off;
+  const unsigned ra0 = p.to_leaves ? (unsigned)((1ull << q.A.depth) - 1) : 0u;
+  const unsigned rb0 = p.to_leaves ? (unsigned)((1ull << q.B.depth) - 1) : 0u;
+  const bool to_leaves = p.to_leaves;
+  const bool culling = q.cfg.culling != 0, enh = q.cfg.enhanced_bounds != 0;
+  unsigned my_culled = 0, my_skipped = 0;
+  uint2* s_node = reinterpret_cast<uint2*>(stage);
+  float* s_key = reinterpret_cast<float*>(stage + kK1Stage * sizeof(uint2));
+  const int lane = threadIdx.x & 31;
+  unsigned per_blk = (n_v + gridDim.x - 1) / gridDim.x;
+  per_blk = (per_blk + 63) & ~63u;
+  const unsigned blk_lo = min(n_v, blockIdx.x * per_blk);
+  const unsigned blk_hi = min(n_v, blk_lo + per_blk);
+  for (unsigned t0 = blk_lo; t0 < blk_hi; t0 += kK1Tile) {
+    const unsigned t1 = min(blk_hi, t0 + kK1Tile);
+    const int R = (int)((t1 - t0 + kExpandThreads - 1) / kExpandThreads);
+    if (threadIdx.x == 0) sh.stage_count = 0;
+    const float ub = load_bound_sq(S);
+    __syncthreads();
+    float upd = kMax ? 0.f : INFINITY;
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const unsigned v = t0 + (unsigned)r * kExpandThreads + threadIdx.x;
+      unsigned keep = 0;
+      float keys[4];
+      uint2 nd = make_uint2(0, 0);
+      if (v < t1) {
+        const float pk = in_key[v >> 2];
+        nd = in_node[v >> 2];
+        if (!owns<kSplit>(q.cfg, nd.x, nd.y, p.da, p.db, la, lb)) {
+          my_skipped += 4;
+        } else if (culling && !survives<kMax>(pk, ub)) {
+          my_culled += 4;
+        } else {
+          const unsigned an = 2 * nd.x + 1 + ((v >> 1) & 1), bn = 2 * nd.y + 1 + (v & 1);
+          Box A[2], B[2];
+          load_children(q.A.box, an, A[0], A[1]);
+          load_children(q.B.box, bn, B[0], B[1]);
+          const Box ca = box_union(A[0], A[1]), cb = box_union(B[0], B[1]);
+          if (culling && !survives<kMax>(pair_key<kMax>(ca, cb), ub)) {
+            my_culled += 4;  // the child pair: its grandchildren are culled with it
+          } else {
+            // bound: the kept child pair's enhanced bound when the
+            // grandchildren are leaves (which emit none), else the most
+            // promising kept grandchild pair's -- both kept non-leaf pairs
+            if (to_leaves) {
+              const float u = pair_update<kMax>(ca, cb, enh);
+              upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
+            }
+            float best = kMax ? -INFINITY : INFINITY;
+            int bc = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float key = pair_key<kMax>(A[c >> 1], B[c & 1]);
+              keys[c] = key;
+              if (culling && !survives<kMax>(key, ub)) {
+                ++my_culled;
+                continue;
+              }
+              keep |= 1u << c;
+              if (improves<kMax>(key, best)) {
+                best = key;
+                bc = c;
+              }
+            }
+            if (keep && !to_leaves) {
+              const float u = pair_update<kMax>(select_box((bc >> 1) != 0, A[1], A[0]),
+                                                select_box((bc & 1) != 0, B[1], B[0]), enh);
+              upd = kMax ? fmaxf(upd, u) : fminf(upd, u);
+            }
+            nd = make_uint2(2 * an + 1 - ra0, 2 * bn + 1 - rb0);  // first grandchild of each side
+          }
+        }
+      }
+      unsigned pos = warp_append(&sh.stage_count, __popc(keep));
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (keep & (1u << c)) {
+          s_node[pos] = make_uint2(nd.x + (c >> 1), nd.y + (c & 1));
+          s_key[pos] = keys[c];
+          ++pos;
+        }
+      }
+    }  // rounds
+    upd = kMax ? warp_max(upd) : warp_min(upd);
+    if (lane == 0) sh.warp_upd[0][threadIdx.x >> 5] = upd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned total = sh.stage_count;
+      sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
+      float u = sh.warp_upd[0][0];
+      for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[0][w]) : fminf(u, sh.warp_upd[0][w]);
+      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u));
+    }
+    __syncthreads();
+    const unsigned total = sh.stage_count;
+    const long long base = (long long)sh.out_base, dir = p.out_dir;
+    uint2* const on = q.fnode + p.out_base;
+    float* const ok = q.fkey + p.out_base;
+    for (unsigned i = threadIdx.x; i < total; i += kExpandThreads) {
+      const long long o = dir * (base + (long long)i);
+      on[o] = s_node[i];
+      ok[o] = s_key[i];
+    }
+    __syncthreads();
+  }
+  sweep_counters(S, sh, p.it, my_culled, my_skipped, kSplit);
+}
+
 // k >= 2 sweep (the narrow early fronts, candidates < front_cap): one thread
 // per candidate of the reference's k-level expansion (query.py:349-451:
 // candidate t -> entry t >> (ka + kb), descendants ((node + 1) << k) - 1 +
@@ -569,6 +695,16 @@ __device__ __noinline__ void plan_sweep(const QArgs& q, TravShared& t, SweepPlan
     while (k < q.cfg.depth_cap && k < rd && 2 * (k + 1) < 62 && (rem >> (62 - 2 * (k + 1))) == 0 &&
            (rem << (2 * (k + 1))) < (unsigned long long)q.cfg.front_cap)
       ++k;
+  // device schedule (GdConfig.schedule >= 0): where the rule above gives
+  // k = 1, a front of at most the threshold's entries expands two levels in
+  // one k2_sweep -- a grid barrier and a front write / re-read per level
+  // saved where the iteration is latency bound.  Only while its <= 16 rem
+  // candidates fit front_hard_cap: then neither of the two reference
+  // iterations it replaces could raise FrontOverflowError either.
+  if (k == 1 && !t.chunked && q.cfg.schedule >= 0 && q.cfg.depth_cap >= 2 && ra >= 2 && rb >= 2 &&
+      rem <= (q.cfg.schedule > 0 ? (unsigned long long)q.cfg.schedule : kK2Front) &&
+      (rem << 4) <= (unsigned long long)q.cfg.front_hard_cap)
+    k = 2;
   const unsigned long long gap = t.hi - t.lo;
   auto fit = [&](int kk) -> unsigned long long {
     const int s = min(kk, ra) + min(kk, rb);
@@ -770,7 +906,9 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
     const SweepPlan& p = t.p[b];  // shared: no register copy of the plan
     if (p.stop) break;
     unsigned long long* cnt = &S->cnt[sweep % 3];
-    if (p.k >= 2)
+    if (p.k == 2 && p.ka == 2 && p.kb == 2)
+      k2_sweep<kMax, kSplit>(q, sh, stage, p, cnt, la, lb);
+    else if (p.k >= 2)
       generic_sweep<kMax, kSplit>(q, sh, p, cnt, la, lb);
     else
       k1_sweep<kMax, kSplit>(q, sh, stage, p, cnt, la, lb);

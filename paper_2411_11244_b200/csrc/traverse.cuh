@@ -15,6 +15,12 @@ constexpr int kExpandThreads = GD_EXPAND_THREADS;
 constexpr int kK1Rounds = 4;                                       // entries / thread / tile (k == 1)
 constexpr int kK1Tile = kExpandThreads * kK1Rounds;
 constexpr int kK1Stage = kK1Tile * 4;                              // staged survivors (<= 4 / entry)
+// device schedule default (GdConfig.schedule == 0): fronts up to this many
+// entries take k = 2 sweeps where the reference rule gives k = 1
+#ifndef GD_K2_FRONT
+#define GD_K2_FRONT (1u << 17)
+#endif
+constexpr unsigned long long kK2Front = GD_K2_FRONT;
 constexpr size_t kExpandDynSmem = kK1Stage * (sizeof(uint2) + sizeof(float));
 __device__ __forceinline__ float load_bound(const QState* S) {
   return __uint_as_float(*reinterpret_cast<const volatile unsigned int*>(&S->bound_bits));

@@ -48,6 +48,13 @@ class EngineConfig:
     # device extension: front arena entries (12 B each); 0 = sized from the
     # free HBM.  Independent of front_hard_cap.
     arena_entries: int = 0
+    # device extension: expansion schedule (GdConfig.schedule).  -1 = the
+    # reference's adaptive_depth exactly (IterationStat.k follows
+    # query.py:266-284); 0 = the device schedule (fronts up to its default
+    # threshold expand two levels per iteration where the reference rule
+    # gives one); > 0 = the device schedule with that threshold in entries.
+    # Distances and witnesses do not depend on it.
+    device_schedule: int = 0
 
     def __post_init__(self):
         if self.front_cap < 4:
@@ -60,6 +67,8 @@ class EngineConfig:
             raise ConfigError(f"batch_size must be >= 4, got {self.batch_size}")
         if self.front_hard_cap < 4:
             raise ConfigError("front_hard_cap must be >= 4")
+        if self.device_schedule < -1 or self.device_schedule >= 1 << 31:
+            raise ConfigError(f"device_schedule must be -1, 0 or a front size < 2^31, got {self.device_schedule}")
         if self.arena_entries < 0:
             raise ConfigError(f"arena_entries must be >= 0, got {self.arena_entries}")
         if isinstance(self.threads, str):
@@ -298,6 +307,7 @@ def _gd_config(cfg: EngineConfig, kind: str, warm_pair, band_cap: int = 0) -> _l
     g.band_cap = band_cap
     g.split_rank, g.split_world, g.split_level = 0, 1, 11
     g.arena_entries = cfg.arena_entries or _auto_arena()
+    g.schedule = cfg.device_schedule
     return g
 
 

@@ -1,5 +1,5 @@
-"""Traversal schedule sweep: the adaptive-depth candidate target C (front_cap)
-and depth_cap vs the rings query's phases (CUDA events, best of 5) and its
+"""Traversal schedule sweep: the device schedule threshold (k = 2 sweeps,
+EngineConfig.device_schedule) and the reference rule's C (front_cap) vs the rings query's phases (CUDA events, best of 5) and its
 per-iteration times.  Usage: python scripts/exp_sched.py [nu nv frame kind]"""
 
 import ctypes as C
@@ -54,16 +54,17 @@ def once(cfg, kind, reps=7):
     return r, best, min(ts), sorted(ts)[len(ts) // 2]
 
 
+VARIANTS = [(-1, 1 << 18, 5), (-1, 1 << 20, 5), (-1, 1 << 22, 5)] + [
+    (sched, 1 << 18, 5) for sched in (1 << 12, 1 << 14, 1 << 16, 1 << 17, 1 << 18, 1 << 19, 1 << 20, 1 << 22, 1 << 26)]
 for kind in kinds:
-    for fc in (1 << 18, 1 << 19, 1 << 20, 1 << 21, 1 << 22, 1 << 23):
-        for dc in (5, 8):
-            cfg = md.EngineConfig(front_cap=fc, depth_cap=dc, front_hard_cap=1 << 28)
-            r, ph, tmin, tmed = once(cfg, kind)
-            its = r.iterations
-            print(json.dumps({
-                "kind": kind, "front_cap": fc, "depth_cap": dc, "query_ms_min": round(tmin, 4),
-                "query_ms_med": round(tmed, 4), "distance": r.distance,
-                "witness": [r.witness.tri_a, r.witness.tri_b],
-                "phases_ms": [round(x, 4) for x in ph[:5]], "expanded": r.expanded_pairs,
-                "iters": [(s.k, s.front_in, round(ph[5 + i], 4) if 5 + i < len(ph) else None)
-                          for i, s in enumerate(its)]}), flush=True)
+    for sched, fc, dc in VARIANTS:
+        cfg = md.EngineConfig(front_cap=fc, depth_cap=dc, front_hard_cap=1 << 28, device_schedule=sched)
+        r, ph, tmin, tmed = once(cfg, kind)
+        its = r.iterations
+        print(json.dumps({
+            "kind": kind, "schedule": sched, "front_cap": fc, "depth_cap": dc, "query_ms_min": round(tmin, 4),
+            "query_ms_med": round(tmed, 4), "distance": r.distance,
+            "witness": [r.witness.tri_a, r.witness.tri_b],
+            "phases_ms": [round(x, 4) for x in ph[:5]], "expanded": r.expanded_pairs,
+            "iters": [(s.k, s.front_in, round(ph[5 + i], 4) if 5 + i < len(ph) else None)
+                      for i, s in enumerate(its)]}), flush=True)

@@ -23,24 +23,43 @@ def _trees(md, a, b):
     return md.build_f12(a), md.build_f12(b)
 
 
+def _device_k(md, n, cfg, rem_a, rem_b, threshold):
+    """The device schedule (GdConfig.schedule >= 0): the reference rule, but
+    k = 2 where it gives 1 for fronts up to the threshold with >= 2 levels
+    left on each tree (traverse.cu plan_sweep)."""
+    k = md.adaptive_depth(n, cfg, max(rem_a, rem_b))
+    if (k == 1 and cfg.depth_cap >= 2 and min(rem_a, rem_b) >= 2 and n <= threshold
+            and 16 * n <= cfg.front_hard_cap):
+        k = 2
+    return k
+
+
 @pytest.mark.parametrize("kind", ["min", "max"])
 @pytest.mark.parametrize("scene", ["rings", "shells"])
-def test_iteration_stats_follow_reference_schedule(md, gpu, kind, scene):
-    """k of every iteration is the reference's adaptive_depth of its front
-    (query.py:266-284); fronts chain (front_out[i] == front_in[i+1]); every
-    candidate is either culled or survives (the last iteration's survivors
-    are the leaf pairs, not a front: front_out 0); the bound is monotone."""
+@pytest.mark.parametrize("schedule", [-1, 0, 1 << 14])
+def test_iteration_stats_follow_schedule(md, gpu, kind, scene, schedule):
+    """schedule -1: k of every iteration is the reference's adaptive_depth of
+    its front (query.py:266-284); >= 0: the device schedule's.  Fronts chain
+    (front_out[i] == front_in[i+1]); every candidate is either culled or
+    survives (the last iteration's survivors are the leaf pairs, not a front:
+    front_out 0); the bound is monotone; the answer does not depend on the
+    schedule."""
     a, b = _scene(md, scene)
     ta, tb = _trees(md, a, b)
-    cfg = md.EngineConfig(front_hard_cap=1 << 30)
-    r = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb, cfg)
+    cfg = md.EngineConfig(front_hard_cap=1 << 30, device_schedule=schedule)
+    run = md.run_min_query if kind == "min" else md.run_max_query
+    r = run(a, b, ta, tb, cfg)
+    ref = run(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30, device_schedule=-1))
+    assert r.distance == ref.distance
+    assert (r.witness.tri_a, r.witness.tri_b) == (ref.witness.tri_a, ref.witness.tri_b)
+    threshold = {-1: 0, 0: 1 << 17}.get(schedule, schedule)
     its = r.iterations
     assert its and its[-1].front_out == 0
     da = db = 0
     total = 0
     for i, s in enumerate(its):
         rem_a, rem_b = ta.depth - da, tb.depth - db
-        assert s.k == md.adaptive_depth(s.front_in, cfg, max(rem_a, rem_b)), (i, s)
+        assert s.k == _device_k(md, s.front_in, cfg, rem_a, rem_b, threshold), (i, s)
         ka, kb = min(s.k, rem_a), min(s.k, rem_b)
         cand = s.front_in << (ka + kb)
         total += cand
@@ -90,22 +109,28 @@ def test_front_hard_cap_semantics_independent_of_arena(md, gpu):
     (breadth first) and with a tiny one (chunked, iteration totals)."""
     a, b = _scene(md, "rings")
     ta, tb = _trees(md, a, b)
-    ok = md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30))
+    ok = md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30, device_schedule=-1))
     cand, da, db = [], 0, 0
     for s in ok.iterations:
         ka, kb = min(s.k, ta.depth - da), min(s.k, tb.depth - db)
         cand.append(s.front_in << (ka + kb))
         da, db = da + ka, db + kb
     cap = max(cand) // 2
+    # the reference schedule and the device schedule (whose k = 2 sweeps
+    # only run while their candidates fit the cap) raise alike
     for arena in (0, 1 << 13):
-        with pytest.raises(md.FrontOverflowError) as ei:
-            md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=cap, arena_entries=arena))
-        assert ei.value.cap == cap and ei.value.candidates > cap
+        for sched in (-1, 0):
+            with pytest.raises(md.FrontOverflowError) as ei:
+                md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=cap, arena_entries=arena,
+                                                               device_schedule=sched))
+            assert ei.value.cap == cap and ei.value.candidates > cap
     # a cap well above every iteration's candidates passes in both layouts
     cap_ok = 4 * max(cand)
     for arena in (0, 1 << 13):
-        r = md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=cap_ok, arena_entries=arena))
-        assert r.distance == ok.distance
+        for sched in (-1, 0):
+            r = md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=cap_ok, arena_entries=arena,
+                                                               device_schedule=sched))
+            assert r.distance == ok.distance
 
 
 def test_arena_too_small_fails_loudly(md, gpu):
