@@ -294,8 +294,8 @@ def max_section(md, _lib, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_d
 def split_section(md, tz, tb, bvh_a, bvh_b, cfg, kind, dist, red_dev, backend, frame=7, reps=5):
     """One query (frame `frame`, every rank the same) split over the N ranks
     (parallel.run_split_query): ownership by ancestor-pair hash, exact parts
-    combined in one all-gather; with and without the in-kernel bound
-    exchange.  Time = max over ranks of the mean wall time per collective
+    combined in one all-gather; the three bound exchanges (none, CUDA IPC
+    peer atomics inside the kernels, all-reduce between traversal rounds).  Time = max over ranks of the mean wall time per collective
     query (the all-gather's synchronisation included), beside the same query
     on one GPU (rank 0's plain query)."""
     import torch
@@ -317,18 +317,19 @@ def split_section(md, tz, tb, bvh_a, bvh_b, cfg, kind, dist, red_dev, backend, f
         torch.cuda.synchronize()
         ts.append(s.elapsed_time(e))
     out = {"frame": frame, "single_gpu_query_ms": round(float(np.median(ts)), 6), "modes": {}}
-    modes = [("rank-local bound", False), ("bound shared over CUDA IPC (peer atomics)", True)]
+    modes = [("rank-local bound", "none"), ("bound shared over CUDA IPC (peer atomics, the default)", "ipc"),
+             ("bound all-reduced between one-sweep traversal rounds", "allreduce")]
     for name, share in modes:
         try:
             for _ in range(2):
-                r = parallel.run_split_query(a, b, bvh_a, bvh_b, kind, cfg, share_bound=share)
+                r = parallel.run_split_query(a, b, bvh_a, bvh_b, kind, cfg, bound_exchange=share)
             assert r.distance == single.distance, (r.distance, single.distance)
             times = []
             for _ in range(reps):
                 dist.barrier()
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                r = parallel.run_split_query(a, b, bvh_a, bvh_b, kind, cfg, share_bound=share)
+                r = parallel.run_split_query(a, b, bvh_a, bvh_b, kind, cfg, bound_exchange=share)
                 times.append((time.perf_counter() - t0) * 1e3)
             mine = torch.tensor([float(np.median(times)), float(r.expanded_pairs)], device=red_dev)
             allv = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 12
+#define GDIST_ABI_VERSION 13
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -282,6 +282,22 @@ int gd_query_round(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, c
 int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                       const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
                       void* stream, void* traversal_done);
+/* Bound-exchange rounds of a split query (the per-round
+ * ncclAllReduce of the bound): enqueue ONLY the traversal -- round 0 starts
+ * the query, a later round continues it -- limited to `sweep_budget` (>= 1)
+ * expansion sweeps per call; a call after the traversal ended is a no-op.
+ * Between calls the caller may combine the ranks' bound cells
+ * (gd_query_bound_device: uint32 bits of a non-negative float, so an
+ * integer MIN / MAX all-reduce is the float one).  gd_query_finish then
+ * enqueues the rest of the traversal (no budget) and the narrow / exact
+ * phases into `result_dev` (may be NULL); collect as after gd_query_async;
+ * a record with `pending` resumes with gd_query_round as usual. */
+int gd_query_traverse(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                      const GdConfig* cfg, void* workspace, size_t workspace_bytes, int round,
+                      int sweep_budget, void* stream);
+int gd_query_finish(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                    const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
+                    void* stream);
 /* Enqueue the device->host copy of the result record followed by
  * min(max_stats, 64) GdIterStat into host_dst (pinned memory of at least
  * sizeof(GdResult) + max_stats * sizeof(GdIterStat) bytes) on `stream`;

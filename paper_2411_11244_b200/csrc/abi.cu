@@ -30,6 +30,10 @@ size_t query_workspace_size(const GdConfig& cfg);
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done,
                  int round = 0);
+void query_traverse(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
+                    void* ws, size_t ws_bytes, int round, int budget, cudaStream_t s);
+void query_finish(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
+                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s);
 const void* query_result_device(const GdConfig& cfg, void* ws);
 void* query_bound_device(const GdConfig& cfg, void* ws);
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
@@ -225,6 +229,24 @@ int gd_query_async_ev(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a
     GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
     query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream),
                 static_cast<cudaEvent_t>(traversal_done));
+  });
+}
+
+int gd_query_traverse(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                      const GdConfig* cfg, void* workspace, size_t workspace_bytes, int round, int sweep_budget,
+                      void* stream) {
+  return guarded([&] {
+    GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
+    query_traverse(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, round, sweep_budget, S(stream));
+  });
+}
+
+int gd_query_finish(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                    const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
+                    void* stream) {
+  return guarded([&] {
+    GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
+    query_finish(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream));
   });
 }
 

@@ -72,7 +72,8 @@ struct alignas(16) QState {
   int rounds;                        // traversal rounds (k_traverse launches) so far
   unsigned long long lo_top, hi_bot; // arena stack tops (entries); gap = [lo_top, hi_bot)
   unsigned long long leaf_off, n_leaf;   // this round's leaf-pair list (arena entries)
-  int leaf_end, _pad0;
+  int leaf_end;
+  int paused;                        // the last traversal launch stopped at its sweep budget (mode 1)
   unsigned long long cand_off, cand_cap; // triangle-pair candidates (k_nfilter -> k_ntest), in the gap
   unsigned long long n_band;
   unsigned long long n_cand;         // triangle-pair candidates (k_nfilter)
@@ -103,6 +104,9 @@ struct QArgs {
   XfF32 xa, xb;  // float32 transforms of ma, mb (xf32_host)
   int profile;    // record per-iteration sweep times (gd_set_profiling)
   int round;      // traversal round (0: the query starts)
+  int mode;       // 0: a round resumes after a leaf chunk; 1: continue a query paused at its sweep budget
+                  //    (a no-op once its traversal ended) -- the split query's bound-exchange rounds
+  int sweep_budget;  // expansion sweeps this launch may run (0 = no limit)
   GdBvh A, B;
   GdConfig cfg;
   QState* S;

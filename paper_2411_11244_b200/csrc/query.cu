@@ -147,17 +147,14 @@ static unsigned refine_grid() {
   return g[dev];
 }
 
+// memset of the grid-barrier counter + the persistent traversal kernel
 template <bool kMax>
-static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_done) {
+static void launch_traverse(const QArgs& q, cudaStream_t s) {
   const int sms = num_sms();
-  auto mark = [&](int i) {
-    if (g_profile) GD_CUDA(cudaEventRecord(g_ev[i], s));
-  };
-  mark(0);
   // the grid-barrier counter must start at 0; everything else is initialised
   // by k_traverse's prologue
   GD_CUDA(cudaMemsetAsync(&q.S->bar, 0, sizeof(unsigned), s));
-  mark(1);
+  if (g_profile) GD_CUDA(cudaEventRecord(g_ev[1], s));
   // persistent traversal: as many blocks as can be co-resident (cooperative
   // launch guarantees it; the grid barrier relies on it); the split-query
   // variant carries the ownership tests
@@ -178,6 +175,16 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
     void* args[] = {const_cast<QArgs*>(&q)};
     GD_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(g), dim3(kExpandThreads), args, kExpandDynSmem, s));
   }
+}
+
+template <bool kMax>
+static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_done) {
+  const int sms = num_sms();
+  auto mark = [&](int i) {
+    if (g_profile) GD_CUDA(cudaEventRecord(g_ev[i], s));
+  };
+  mark(0);
+  launch_traverse<kMax>(q, s);  // records g_ev[1] between the memset and the kernel
   // the node boxes are read by k_traverse only: a refit for the next frame
   // may start once this event has fired
   if (traversal_done) GD_CUDA(cudaEventRecord(traversal_done, s));
@@ -233,6 +240,8 @@ static QArgs make_args(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const
   q.arena = L.arena;
   q.band_cap = L.band_cap;
   q.result = result_dev;  // nullptr: the record stays in the state block (QState::res)
+  q.mode = 0;
+  q.sweep_budget = 0;
   return q;
 }
 
@@ -250,6 +259,40 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
     launch_query<true>(q, s, traversal_done);
   else
     launch_query<false>(q, s, traversal_done);
+}
+
+// Bound-exchange rounds of a split query: the traversal
+// alone, at most `budget` sweeps per launch (mode 1: a launch continues the
+// paused query, a no-op once its traversal ended); the caller combines the
+// ranks' bound cells between launches.  query_finish runs the rest of the
+// traversal without a budget, then the narrow and exact phases.
+void query_traverse(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
+                    void* ws, size_t ws_bytes, int round, int budget, cudaStream_t s) {
+  validate(a, b, cfg);
+  GD_CHECK(round >= 0 && budget >= 1, GD_ERR_INVALID, "round must be >= 0 and sweep_budget >= 1");
+  QArgs q = make_args(ma, mb, a, b, cfg, ws, ws_bytes, nullptr);
+  q.round = round;
+  q.mode = 1;
+  q.sweep_budget = budget;
+  if (cfg.kind == 1)
+    launch_traverse<true>(q, s);
+  else
+    launch_traverse<false>(q, s);
+  GD_CUDA(cudaGetLastError());
+  count_launches(1);
+}
+
+void query_finish(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
+                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s) {
+  validate(a, b, cfg);
+  QArgs q = make_args(ma, mb, a, b, cfg, ws, ws_bytes, result_dev);
+  q.round = 1;
+  q.mode = 1;
+  if (g_profile) g_last_state = q.S;
+  if (cfg.kind == 1)
+    launch_query<true>(q, s, nullptr);
+  else
+    launch_query<false>(q, s, nullptr);
 }
 
 static_assert(offsetof(QState, stats) == offsetof(QState, res) + sizeof(GdResult),

@@ -67,6 +67,7 @@ __device__ void init_query(const QArgs& q) {
   S->sp = 0;
   S->chunked = 0;
   S->pending = 0;
+  S->paused = 0;
   S->rounds = 0;
   S->lo_top = 1;  // the root entry
   S->hi_bot = q.arena;
@@ -406,7 +407,7 @@ __device__ __forceinline__ void k1_sweep(const QArgs& q, ExpandShared& sh, unsig
       sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
       float u = sh.warp_upd[0][0];
       for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[0][w]) : fminf(u, sh.warp_upd[0][w]);
-      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u));
+      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u), ub);
     }
     __syncthreads();
     const unsigned total = sh.stage_count;
@@ -554,7 +555,7 @@ __device__ __forceinline__ void k2_sweep(const QArgs& q, ExpandShared& sh, unsig
       sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
       float u = sh.warp_upd[0][0];
       for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[0][w]) : fminf(u, sh.warp_upd[0][w]);
-      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u));
+      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u), ub);
     }
     __syncthreads();
     const unsigned total = sh.stage_count;
@@ -633,7 +634,7 @@ __device__ __forceinline__ void generic_sweep(const QArgs& q, ExpandShared& sh, 
       sh.out_base = total ? (atomicAdd(n_out, (unsigned long long)total) & ((1ull << kArriveShift) - 1)) : 0ull;
       float u = sh.warp_upd[0][0];
       for (int w = 1; w < kExpandThreads / 32; ++w) u = kMax ? fmaxf(u, sh.warp_upd[0][w]) : fminf(u, sh.warp_upd[0][w]);
-      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u));
+      if (kMax ? u > 0.f : u < INFINITY) commit_bound<kMax>(q, sqrtf(u), ub);
     }
     __syncthreads();
     if (keep) {
@@ -849,6 +850,12 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
   __shared__ QArgs qs;  // the out-of-line functions' view of the arguments (shared, not a local copy)
   extern __shared__ __align__(16) unsigned char stage[];
   const volatile QState* V = S;
+  // mode 1 (bound-exchange rounds): a later launch continues a query its
+  // sweep budget paused, and does nothing once the traversal has ended.
+  // Every block reads `paused` before the first grid barrier; block 0
+  // rewrites it only after its last one.
+  const bool cont = q.mode == 1 && q.round > 0;
+  if (cont && !V->paused) return;
   if (threadIdx.x == 0) qs = q;
   const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
   if (blockIdx.x == 0) {
@@ -864,7 +871,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
         S->tot_in[i] = 0;
         S->tot_out[i] = 0;
       }
-    } else if (threadIdx.x == 0) {
+    } else if (threadIdx.x == 0 && !cont) {
       resume_round(q);
     }
     if (threadIdx.x < 3) S->cnt[threadIdx.x] = 0;
@@ -875,6 +882,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
     t.tot_in[i] = V->tot_in[i];
     t.tot_out[i] = V->tot_out[i];
   }
+  __syncthreads();  // thread 0's plan_sweep reads the totals other threads copied (racecheck)
   if (threadIdx.x == 0) {
     t.sp = V->sp;
     for (int i = 0; i < t.sp; ++i) {
@@ -921,7 +929,12 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
     if (threadIdx.x == 0) {
       SweepPlan& nx = t.p[b ^ 1];
       commit_sweep<kMax>(qs, t, p, nx, n_out, rec);
-      if (!nx.stop) plan_sweep<kMax>(qs, t, nx, rec);
+      if (!nx.stop) {
+        if (q.sweep_budget > 0 && sweep >= (unsigned)q.sweep_budget)
+          nx.stop = 4;  // paused: the stack is saved below, the next mode-1 launch continues
+        else
+          plan_sweep<kMax>(qs, t, nx, rec);
+      }
     }
     __syncthreads();
     b ^= 1;
@@ -946,10 +959,11 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
       S->leaf_end = t.leaf_end;
     }
     S->pending = stop == 2 && t.sp > 0;
+    S->paused = stop == 4;
     // the triangle-pair candidates of this round's narrow phase use the gap
     S->cand_off = t.lo;
     S->cand_cap = t.hi - t.lo;
-    S->rounds = q.round + 1;
+    if (q.mode == 0 || q.round == 0) S->rounds = q.round + 1;
     unsigned long long skipped = 0;
     if (kSplit)
       for (int i = 0; i < t.iter; ++i) skipped += V->skip_it[i];

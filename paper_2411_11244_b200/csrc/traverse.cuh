@@ -47,12 +47,17 @@ __device__ __forceinline__ void commit_bound(QState* S, float v) {
 // the same, also applied to the other ranks' bound cells of a split query
 // (GdConfig.peer_bounds: their workspaces mapped over NVLink).  A bound is an
 // achieved distance +- the common slack, valid for every rank's sub-query.
+// The remote atomics are sent only when the bound improves on `snap_sq`
+// (the caller's tile snapshot of the cell, squared): once the bounds have
+// converged, tiles send nothing over the links.
 template <bool kMax>
-__device__ __forceinline__ void commit_bound(const QArgs& q, float v) {
+__device__ __forceinline__ void commit_bound(const QArgs& q, float v, float snap_sq = kMax ? -1.f : INFINITY) {
   QState* S = q.S;
   commit_bound<kMax>(S, v);
   if (q.cfg.n_peers > 0) {
-    const unsigned bits = __float_as_uint(fmaxf(kMax ? v - S->slack : v + S->slack, 0.f));
+    const float nb = fmaxf(kMax ? v - S->slack : v + S->slack, 0.f);
+    if (kMax ? !(nb * nb > snap_sq) : !(nb * nb < snap_sq)) return;
+    const unsigned bits = __float_as_uint(nb);
     unsigned* const* peers = static_cast<unsigned* const*>(q.cfg.peer_bounds);
     for (int i = 0; i < q.cfg.n_peers; ++i) {
       if (kMax)

@@ -12,12 +12,17 @@ query.py:426-433 parallelises only over CPU threads).
   part independently -- its own bound is a valid global bound, so every pair
   that can attain the optimum survives on its owner -- and the exact answers
   are combined with the reference's lexicographic witness rule
-  (query.py:205-220) in one all-gather.  With `share_bound` (the default when the
-  ranks share a node) the ranks' bound cells are mapped into each other over
-  CUDA IPC (NVLink peer memory) and every bound a rank commits is applied to
-  all of them with a system-scope atomic, inside the kernels -- the
-  per-round bound exchange of SURVEY.md 8(e) without a host round trip, so
-  every rank culls with the best bound found anywhere.
+  (query.py:205-220) in one all-gather.  The ranks' bounds are exchanged
+  while they traverse (`bound_exchange`):
+    "ipc" (the default for a process group): the bound cells are mapped into
+      each other over CUDA IPC (NVLink peer memory); a rank that improves on
+      its tile's bound snapshot also applies the bound to every peer cell with
+      a system-scope atomic, inside the kernels -- no round, no host sync;
+    "allreduce" (SURVEY.md 8(e) as written; the fallback when IPC mapping
+      fails): the traversal runs in rounds of one expansion sweep per launch
+      and the 4-byte bound cells are all-reduced (MIN / MAX) between rounds
+      with torch.distributed (NCCL on GPUs), all on the stream;
+    "none": every rank culls with its own bound only.
 
 The collective plumbing is torch.distributed (NCCL on GPUs, gloo in the CPU
 tests); the per-frame / per-part compute is libgdist's.
@@ -243,7 +248,11 @@ def _link_bounds(pq, rank: int, world: int, group=None):
 
 def _split_plan(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level, group):
     """The cached per-rank plan of a bound-sharing split query (private
-    workspace whose bound cell is linked to the other ranks' once)."""
+    workspace whose bound cell is linked to the other ranks' once), or None
+    when some rank could not map the others' cells (collective decision)."""
+    import torch
+
+    from . import _lib
     from .query import PreparedQuery
 
     key = (id(bvh_a), id(bvh_b), cfg, kind, rank, world, split_level, id(group))
@@ -251,10 +260,55 @@ def _split_plan(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_leve
     if ent is None or ent[0] is not bvh_a or ent[1] is not bvh_b:
         pq = PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind, private_workspace=True)
         pq.g_cfg.split_rank, pq.g_cfg.split_world, pq.g_cfg.split_level = int(rank), int(world), int(split_level)
-        _link_bounds(pq, rank, world, group)
+        try:
+            _link_bounds(pq, rank, world, group)
+            ok = 1
+        except RuntimeError:
+            ok = 0
+        dist = _dist()
+        flag = torch.tensor([ok], dtype=torch.int32)
+        if dist.get_backend(group) == "nccl":
+            flag = flag.cuda()
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if not int(flag.item()):
+            for base in getattr(pq, "_peer_bases", []):
+                _lib.lib().gd_ipc_close(base)
+            return None
         ent = (bvh_a, bvh_b, pq)
         _SPLIT_PLANS[key] = ent
     return ent[2].bind(mesh_a, mesh_b)
+
+
+def _allreduce_rounds(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level, group,
+                      sweep_budget: int = 1):
+    """This rank's part with the bound all-reduced between traversal rounds
+    (SURVEY.md 8(e)): round r runs at most `sweep_budget` expansion sweeps
+    (gd_query_traverse), then the ranks' 4-byte bound cells are combined
+    with an all-reduce MIN (min query) / MAX (max query) -- the cells hold
+    float bits of non-negative bounds, so the int32 order is the float order
+    -- all enqueued on the stream (NCCL) without a host sync.  Every rank
+    runs the same number of rounds (one per level of the deeper tree, the
+    most sweeps a breadth-first traversal takes); rounds after a rank's
+    traversal ended are no-ops on it.  Then the unbudgeted rest (a chunked
+    traversal) and the narrow / exact phases."""
+    from .query import PreparedQuery
+
+    dist = _dist()
+    pq = PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, kind)
+    pq.g_cfg.split_rank, pq.g_cfg.split_world, pq.g_cfg.split_level = int(rank), int(world), int(split_level)
+    cell = pq.bound_cell()
+    nccl = dist.get_backend(group) == "nccl"
+    op = dist.ReduceOp.MAX if kind == "max" else dist.ReduceOp.MIN
+    for r in range(max(bvh_a.depth, bvh_b.depth, 1)):
+        pq.traverse(r, sweep_budget)
+        if nccl:
+            dist.all_reduce(cell, op=op, group=group)
+        else:  # gloo (CPU tests, ranks sharing a GPU): through host memory
+            host = cell.cpu()
+            dist.all_reduce(host, op=op, group=group)
+            cell.copy_(host)
+    pq.finish()
+    return pq.collect()
 
 
 def release_split_plans(group=None):
@@ -274,19 +328,25 @@ def release_split_plans(group=None):
     _SPLIT_PLANS.clear()
 
 
+BOUND_EXCHANGES = ("ipc", "allreduce", "none")
+
+
 def run_split_query(mesh_a, mesh_b, bvh_a, bvh_b, kind: str = "min", cfg=None, group=None, split_level: int | None = None,
-                    rank: int | None = None, world: int | None = None, share_bound: bool = False):
+                    rank: int | None = None, world: int | None = None, share_bound: bool | None = None,
+                    bound_exchange: str | None = None):
     """One query split over the ranks of `group` (or, with explicit
     rank / world, one part of it -- e.g. to emulate the split on one GPU).
 
     Each rank expands only the node pairs whose ancestor pair at tree level
     `split_level` hashes to it (gdist.h GdConfig.split_*), and the exact
-    per-rank answers are combined with the reference's witness rule.  With
-    `share_bound` (and a process group spanning the ranks) the ranks' bound
-    cells are linked over CUDA IPC / NVLink (GdConfig.peer_bounds), so each
-    part culls with the global best bound.  The returned QueryResult carries
-    the global distance / witness and this rank's own iteration statistics.
-    Collective: every rank of the group calls it with the same arguments."""
+    per-rank answers are combined with the reference's witness rule.  The
+    ranks' bounds are exchanged per `bound_exchange` (module docstring):
+    "ipc" by default when a process group spans the ranks ("allreduce" if
+    the IPC mapping fails), "none" for a single part.  `share_bound` is the
+    older switch: True = "ipc", False = "none".  The returned QueryResult
+    carries the global distance / witness and this rank's own iteration
+    statistics.  Collective: every rank of the group calls it with the same
+    arguments."""
     import torch
 
     from .query import EngineConfig, QueryResult, Witness
@@ -298,11 +358,26 @@ def run_split_query(mesh_a, mesh_b, bvh_a, bvh_b, kind: str = "min", cfg=None, g
     cfg = cfg or EngineConfig()
     if split_level is None:
         split_level = default_split_level(bvh_a, bvh_b)
-    if share_bound and grouped and world > 1:
+    if bound_exchange is None:
+        if share_bound is not None:
+            bound_exchange = "ipc" if share_bound else "none"
+        else:
+            bound_exchange = "ipc"
+    if bound_exchange not in BOUND_EXCHANGES:
+        raise ValueError(f"bound_exchange must be one of {BOUND_EXCHANGES}, got {bound_exchange!r}")
+    if not (grouped and world > 1):
+        bound_exchange = "none"  # one part alone: nobody to exchange with
+    if bound_exchange == "ipc":
         # every rank has finished its previous split query (the all-gather
         # below), so no peer cell is still in use by another query
-        r = _split_plan(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level, group).run()
-    else:
+        pq = _split_plan(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level, group)
+        if pq is None:  # the cells could not be mapped on some rank
+            bound_exchange = "allreduce"
+        else:
+            r = pq.run()
+    if bound_exchange == "allreduce":
+        r = _allreduce_rounds(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level, group)
+    elif bound_exchange == "none":
         r = split_part(mesh_a, mesh_b, bvh_a, bvh_b, kind, cfg, rank, world, split_level)
     w = r.witness
     mine = torch.tensor([r.distance, -1.0 if w is None else w.tri_a, -1.0 if w is None else w.tri_b,

@@ -384,6 +384,34 @@ class PreparedQuery:
                                                 C.byref(self.g_b), C.byref(self.g_cfg), _lib.ptr(self.ws),
                                                 self.ws.numel(), None, stream or _lib.stream_ptr(), ev), "query")
 
+    # -- bound-exchange rounds (split query)
+    def traverse(self, round: int, sweep_budget: int = 1, stream=None):
+        """Enqueue only the traversal, at most `sweep_budget` expansion
+        sweeps (round 0 starts the query, later rounds continue it; no-op
+        once it ended) -- gd_query_traverse.  Between rounds the caller may
+        combine the ranks' bound cells (`bound_cell`)."""
+        _lib.check(_lib.lib().gd_query_traverse(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a),
+                                                C.byref(self.g_b), C.byref(self.g_cfg), _lib.ptr(self.ws),
+                                                self.ws.numel(), int(round), int(sweep_budget),
+                                                stream or _lib.stream_ptr()), "query_traverse")
+
+    def finish(self, stream=None):
+        """Enqueue the rest of the traversal and the narrow / exact phases
+        (gd_query_finish); collect() as after launch()."""
+        _lib.check(_lib.lib().gd_query_finish(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a),
+                                              C.byref(self.g_b), C.byref(self.g_cfg), _lib.ptr(self.ws),
+                                              self.ws.numel(), None, stream or _lib.stream_ptr()), "query_finish")
+
+    def bound_cell(self):
+        """The workspace's bound cell as a 1-element int32 CUDA tensor view
+        (float32 bits of a non-negative bound: integer MIN / MAX order is the
+        float order), for an all-reduce between traversal rounds."""
+        p = C.c_void_p()
+        _lib.check(_lib.lib().gd_query_bound_device(C.byref(self.g_cfg), _lib.ptr(self.ws), C.byref(p)),
+                   "query_bound_device")
+        off = p.value - self.ws.data_ptr()
+        return self.ws[off:off + 4].view(_lib.torch().int32)
+
     def collect(self, stream=None) -> QueryResult:
         s = stream or _lib.stream_ptr()
         L = _lib.lib()

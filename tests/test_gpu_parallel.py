@@ -1,8 +1,8 @@
 """Multi-GPU paths on one GPU (gpurun provides one): the split query's parts
 run one after another and combine to the single-GPU answer; two processes
-sharing cuda:0 over a gloo group run the distributed split query (with the
-ranks' bound cells linked over CUDA IPC, and without) and the sharded frame
-sequence end to end."""
+sharing cuda:0 over a gloo group run the distributed split query (bound cells
+linked over CUDA IPC, all-reduced between budgeted traversal rounds, and not
+exchanged) and the sharded frame sequence end to end."""
 
 import os
 import socket
@@ -66,11 +66,14 @@ def _worker(rank, world, port, q):
         out = {}
         for kind in ("min", "max"):
             for rep in range(2):  # the linked plan is cached: the second call reuses the IPC mapping
-                r = md.run_split_query(a, b, ta, tb, kind, share_bound=True)  # bound cells linked over CUDA IPC
+                r = md.run_split_query(a, b, ta, tb, kind)  # default: bound cells linked over CUDA IPC
                 out[kind] = (r.distance, r.witness.tri_a, r.witness.tri_b, r.witness.point_a.tolist())
             loc = md.run_split_query(a, b, ta, tb, kind, share_bound=False)
             out[kind + "_local"] = (loc.distance, loc.witness.tri_a, loc.witness.tri_b, loc.witness.point_a.tolist())
-            out[kind + "_work"] = (r.expanded_pairs, loc.expanded_pairs)
+            # the per-round all-reduce of the bound cells (SURVEY.md 8(e) as written)
+            ar = md.run_split_query(a, b, ta, tb, kind, bound_exchange="allreduce")
+            out[kind + "_allreduce"] = (ar.distance, ar.witness.tri_a, ar.witness.tri_b, ar.witness.point_a.tolist())
+            out[kind + "_work"] = (r.expanded_pairs, loc.expanded_pairs, ar.expanded_pairs)
         tz, tbase = md.ring_pair_base(60, 30)
         za, zb = md.build_f12(tz), md.build_f12(tbase)
         xfs = [md.ring_frame_transforms(f) for f in range(0, 70, 10)]
@@ -118,7 +121,50 @@ def test_two_processes_gloo(md, gpu):
             assert out[kind][:3] == (r.distance, r.witness.tri_a, r.witness.tri_b), (rank, kind)
             assert out[kind][3] == r.witness.point_a.tolist()
             assert out[kind + "_local"] == out[kind], (rank, kind)
+            assert out[kind + "_allreduce"] == out[kind], (rank, kind)
+            # exchanging bounds never makes a rank's part bigger than culling
+            # with its own bound alone (same cells, tighter or equal bound)
+            ipc, local, ar = out[kind + "_work"]
+            assert ipc <= local * 1.02 and ar <= local * 1.02, (rank, kind, out[kind + "_work"])
         assert np.array_equal(np.asarray(seq), np.asarray(want_seq, dtype=np.float64)), rank
+
+
+@pytest.mark.parametrize("budget", [1, 2, 5])
+@pytest.mark.parametrize("scene", [0, 2])
+def test_budgeted_traversal_rounds(md, gpu, scene, budget):
+    """gd_query_traverse / gd_query_finish (the allreduce mode's rounds):
+    a traversal paused every `budget` sweeps and continued, with more rounds
+    than it needs (the extra ones are no-ops), returns the one-launch answer
+    and statistics; the bound cell view reads the bound; a small arena's
+    chunked traversal still completes through the pending rounds."""
+    import struct
+
+    from paper_2411_11244_b200 import query as Q
+
+    kind_, params = SCENES[scene]
+    a, b = md.gen_scene(kind_, params)
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    for kind in ("min", "max"):
+        for arena in (0, 1 << 11):
+            cfg = md.EngineConfig(front_hard_cap=1 << 28, arena_entries=arena, device_schedule=-1)
+            want = (md.run_min_query if kind == "min" else md.run_max_query)(a, b, ta, tb, cfg)
+            pq = Q.PreparedQuery(a, b, ta, tb, cfg, kind, private_workspace=True)
+            for r in range(ta.depth + 3):
+                pq.traverse(r, budget)
+            bits = int(pq.bound_cell().item()) & 0xFFFFFFFF
+            bound = struct.unpack("<f", struct.pack("<I", bits))[0]
+            pq.finish()
+            got = pq.collect()
+            assert got.distance == want.distance, (kind, arena, budget)
+            assert (got.witness.tri_a, got.witness.tri_b) == (want.witness.tri_a, want.witness.tri_b)
+            its = got.iterations
+            assert its and its[0].front_in == 1 and its[-1].front_out == 0
+            da = db = 0
+            for s in its:
+                da, db = da + min(s.k, ta.depth - da), db + min(s.k, tb.depth - db)
+            assert (da, db) == (ta.depth, tb.depth)
+            # the cell holds the slack-carrying bound: at or beyond the answer
+            assert (bound >= want.distance) if kind == "min" else (bound <= want.distance)
 
 
 def test_sequence_pipelining_and_inflight_queries(md, gpu):
