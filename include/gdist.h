@@ -298,6 +298,21 @@ int gd_query_traverse(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a
 int gd_query_finish(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                     const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
                     void* stream);
+/* Frame graph: refit A and / or B, then n_queries
+ * (<= 8) single-GPU queries (cfgs[i] on workspaces[i]) each followed, when
+ * host_dst[i] is not NULL, by the copy of its result record + max_stats
+ * GdIterStat into host_dst[i] (pinned) -- captured ONCE as a CUDA graph.
+ * gd_frame_graph_launch replays it on `stream` for new rigid transforms of
+ * the same meshes (same base vertices; mesh_a / mesh_b carry the frame's
+ * rot / trans): one call per frame.  A record with `pending` (a chunked
+ * traversal) resumes with gd_query_round as after gd_query_async.  The
+ * workspaces and host buffers stay bound to the graph until destroy. */
+int gd_frame_graph_create(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                          int n_queries, const GdConfig* cfgs, void* const* workspaces,
+                          const size_t* workspace_bytes, void* const* host_dst, int max_stats, int refit_a,
+                          int refit_b, void** graph_out);
+int gd_frame_graph_launch(void* graph, const GdMesh* mesh_a, const GdMesh* mesh_b, void* stream);
+int gd_frame_graph_destroy(void* graph);
 /* Enqueue the device->host copy of the result record followed by
  * min(max_stats, 64) GdIterStat into host_dst (pinned memory of at least
  * sizeof(GdResult) + max_stats * sizeof(GdIterStat) bytes) on `stream`;

@@ -23,10 +23,10 @@ _EXPORTS = {
     "errors": "ConfigError DegenerateTriangleError FrontOverflowError MeshDistError ObjParseError SceneError "
               "SizeGuardError TightnessError TopologyMismatchError",
     "mesh": "RigidTransform TriangleMesh apply_transform load_obj relative_mesh",
-    "query": "EngineConfig Front FrontEntry IterationStat PreparedQuery QueryResult QueryState Witness "
+    "query": "EngineConfig FrameGraph Front FrontEntry IterationStat PreparedQuery QueryResult QueryState Witness "
              "adaptive_depth brute_force_max brute_force_min expand_front process_leaf_pair run_dfs_baseline "
              "run_max_query run_min_query",
-    "parallel": "run_sequence run_split_query",
+    "parallel": "run_sequence run_sequence_minmax run_split_query",
     "scenes": "gen_scene ring_frame_transforms ring_pair_base scene_kinds torus_mesh",
 }
 for _module, _names in _EXPORTS.items():

@@ -34,6 +34,11 @@ void query_traverse(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const Gd
                     void* ws, size_t ws_bytes, int round, int budget, cudaStream_t s);
 void query_finish(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                   void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s);
+void* frame_graph_create(const GdMesh& ma, const GdMesh& mb, const GdBvh& A, const GdBvh& B, int n_queries,
+                         const GdConfig* cfgs, void* const* wss, const size_t* ws_bytes, void* const* host_dst,
+                         int max_stats, int refit_a, int refit_b);
+void frame_graph_launch(void* h, const GdMesh& ma, const GdMesh& mb, cudaStream_t s);
+void frame_graph_destroy(void* h);
 const void* query_result_device(const GdConfig& cfg, void* ws);
 void* query_bound_device(const GdConfig& cfg, void* ws);
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
@@ -248,6 +253,29 @@ int gd_query_finish(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, 
     GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
     query_finish(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, result_dev, S(stream));
   });
+}
+
+int gd_frame_graph_create(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
+                          int n_queries, const GdConfig* cfgs, void* const* workspaces,
+                          const size_t* workspace_bytes, void* const* host_dst, int max_stats, int refit_a,
+                          int refit_b, void** graph_out) {
+  return guarded([&] {
+    GD_CHECK(mesh_a && mesh_b && a && b && graph_out && (n_queries == 0 || (cfgs && workspaces && workspace_bytes)),
+             GD_ERR_INVALID, "null argument");
+    *graph_out = frame_graph_create(*mesh_a, *mesh_b, *a, *b, n_queries, cfgs, workspaces, workspace_bytes,
+                                    host_dst, max_stats, refit_a, refit_b);
+  });
+}
+
+int gd_frame_graph_launch(void* graph, const GdMesh* mesh_a, const GdMesh* mesh_b, void* stream) {
+  return guarded([&] {
+    GD_CHECK(graph && mesh_a && mesh_b, GD_ERR_INVALID, "null argument");
+    frame_graph_launch(graph, *mesh_a, *mesh_b, S(stream));
+  });
+}
+
+int gd_frame_graph_destroy(void* graph) {
+  return guarded([&] { frame_graph_destroy(graph); });
 }
 
 int gd_query_result_async(const GdConfig* cfg, void* workspace, void* host_dst, int max_stats, void* stream) {

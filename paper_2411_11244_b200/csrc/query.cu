@@ -245,6 +245,37 @@ static QArgs make_args(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const
   return q;
 }
 
+// Frame graphs (graph.cu): the query kernels of a captured frame take one
+// QArgs; a replay for new rigid transforms rewrites its meshes' transforms
+// (the same derivation as make_args).
+bool is_query_kernel(const void* f) {
+  const void* ks[] = {(const void*)k_traverse_min,         (const void*)k_traverse_max,
+                      (const void*)k_traverse_min_split,   (const void*)k_traverse_max_split,
+                      (const void*)k_nfilter<false, false>, (const void*)k_nfilter<false, true>,
+                      (const void*)k_nfilter<true, false>,  (const void*)k_nfilter<true, true>,
+                      (const void*)k_ntest<false>,          (const void*)k_refine<false>,
+                      (const void*)k_refine<true>};
+  for (const void* k : ks)
+    if (k == f) return true;
+  return false;
+}
+
+void retransform(QArgs& q, const GdMesh& ma, const GdMesh& mb) {
+  GD_CHECK(ma.vtx == q.ma.vtx && mb.vtx == q.mb.vtx && ma.m == q.ma.m && mb.m == q.mb.m, GD_ERR_TOPOLOGY,
+           "a frame graph replays the meshes it was captured with (same base vertices), moved");
+  q.ma = ma;
+  q.mb = mb;
+  if (q.cfg.frame == 1) {
+    q.xa = xf32_host(relative_mesh(ma, mb));
+    GdMesh id = mb;
+    id.has_xf = 0;
+    q.xb = xf32_host(id);
+  } else {
+    q.xa = xf32_host(ma);
+    q.xb = xf32_host(mb);
+  }
+}
+
 // round 0 starts the query; round r > 0 resumes a query whose record says
 // `pending` (its last round ended with a leaf chunk while levels remained)
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,

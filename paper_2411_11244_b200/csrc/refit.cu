@@ -249,6 +249,8 @@ void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CUDA(cudaGetLastError());
 }
 
+const void* refit_kernel() { return (const void*)k_refit; }  // frame graphs (graph.cu)
+
 void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.m == T.n_tris, GD_ERR_TOPOLOGY,
            "refit mesh has " + std::to_string(m.m) + " triangles, tree was built over " + std::to_string(T.n_tris));

@@ -93,8 +93,52 @@ def run_frames(n_frames: int, frame_fn, group=None, device=None) -> np.ndarray:
     return gather_frames(n_frames, local, group, device)
 
 
+def run_sequence_minmax(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kinds=("min", "max"), cfg=None,
+                        group=None) -> dict:
+    """Config 3: every kind in `kinds` (min and max distance) at every frame
+    of a rigid-motion sequence, frames sharded over the ranks like
+    run_sequence.  Each frame -- refit A, refit B, the queries and the copies
+    of their records -- is ONE CUDA graph replay (query.FrameGraph); two
+    graphs alternate, so the host reads frame f's records while frame f + 1
+    runs.  Returns {kind: (n_frames, 3) array of (distance, tri_a, tri_b)}
+    on every rank."""
+    from .mesh import apply_transform
+    from .query import FrameGraph
+
+    rank, world = world_info(group)
+    mine = list(frames_of_rank(len(transforms), rank, world))
+    local = {k: {} for k in kinds}
+
+    def moved(f):
+        xa, xb = transforms[f]
+        return (mesh_a if xa is None else apply_transform(mesh_a, xa),
+                mesh_b if xb is None else apply_transform(mesh_b, xb))
+
+    def take(f, g):
+        for k, r in g.results().items():
+            w = r.witness
+            local[k][f] = (r.distance, -1 if w is None else w.tri_a, -1 if w is None else w.tri_b)
+
+    graphs, pending = [], None
+    try:
+        for i, f in enumerate(mine):
+            a, b = moved(f)
+            if len(graphs) < 2:
+                graphs.append(FrameGraph(a, b, bvh_a, bvh_b, kinds, cfg))
+            g = graphs[i % 2].launch(a, b)
+            if pending is not None:
+                take(*pending)
+            pending = (f, g)
+        if pending is not None:
+            take(*pending)
+    finally:
+        for g in graphs:
+            g.close()
+    return {k: gather_frames(len(transforms), local[k], group) for k in kinds}
+
+
 def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cfg=None, group=None,
-                 pipelined: bool = True, frame: str = "world", warm: bool = False) -> np.ndarray:
+                 pipelined: bool = True, frame: str = "world", warm: bool = False, graph: bool = False) -> np.ndarray:
     """Distance over a rigid-motion sequence, frames sharded over the ranks.
 
     transforms: list of (xf_a, xf_b) RigidTransform pairs (either may be
@@ -113,7 +157,9 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
     frame f's narrow and exact phases, and two query plans are in flight so
     the host never waits on the GPU between frames.
     warm: seed each frame's bound with the previous frame's witness pair on
-    the device (PreparedQuery.seed_from; temporal coherence, exact)."""
+    the device (PreparedQuery.seed_from; temporal coherence, exact).
+    graph: each frame (refits + query + record copy) is one CUDA graph
+    replay (run_sequence_minmax); world frame, no warm start."""
     import torch
 
     from .bvh import refit
@@ -122,6 +168,10 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
 
     if frame not in ("world", "b-local"):
         raise ValueError(f"frame must be 'world' or 'b-local', got {frame!r}")
+    if graph:
+        if frame != "world" or warm:
+            raise ValueError("graph=True runs world-frame frames without warm start")
+        return run_sequence_minmax(mesh_a, mesh_b, bvh_a, bvh_b, transforms, (kind,), cfg, group)[kind]
     cfg = cfg or EngineConfig()
     rank, world = world_info(group)
     mine = list(frames_of_rank(len(transforms), rank, world))

@@ -482,6 +482,90 @@ class PreparedQuery:
         return _result(self.kind, r, stats)
 
 
+class FrameGraph:
+    """One frame of a rigid-motion sequence -- refit both trees, then one
+    query per kind in `kinds` with the copy of each result record to pinned
+    host memory -- captured once as a CUDA graph (gd_frame_graph_create,
+    SURVEY.md 8(f) row 1) and replayed per frame for the frame's moved
+    meshes (same base meshes, any rigid transforms): one host call per frame.
+    The queries use private workspaces bound to the graph.  Single GPU
+    (no split query)."""
+
+    def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, kinds=("min", "max"), cfg: EngineConfig | None = None):
+        torch = _lib.torch()
+        cfg = cfg or EngineConfig()
+        if not kinds or any(k not in ("min", "max") for k in kinds):
+            raise ValueError(f"kinds must be a non-empty sequence of 'min' / 'max', got {kinds!r}")
+        self.kinds = tuple(kinds)
+        self.trees = (bvh_a, bvh_b)
+        self._roots = (mesh_a._root, mesh_b._root)
+        # stage the base vertices (and lay out the leaves) outside the capture
+        bvh_a.ensure_device(mesh_a)
+        bvh_b.ensure_device(mesh_b)
+        self.plans = [PreparedQuery(mesh_a, mesh_b, bvh_a, bvh_b, cfg, k, private_workspace=True) for k in self.kinds]
+        nbytes = C.sizeof(_lib.GdResult) + _MAX_STATS * C.sizeof(_lib.GdIterStat)
+        self._pinned = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in self.kinds]
+        n = len(self.kinds)
+        cfgs = (_lib.GdConfig * n)(*[p.g_cfg for p in self.plans])
+        wss = (C.c_void_p * n)(*[p.ws.data_ptr() for p in self.plans])
+        sizes = (C.c_size_t * n)(*[p.ws.numel() for p in self.plans])
+        dst = (C.c_void_p * n)(*[t.data_ptr() for t in self._pinned])
+        g_ma, g_mb = mesh_a.device_view(), mesh_b.device_view()
+        h = C.c_void_p()
+        _lib.check(_lib.lib().gd_frame_graph_create(C.byref(g_ma), C.byref(g_mb), C.byref(bvh_a.device_view()),
+                                                    C.byref(bvh_b.device_view()), n, cfgs, wss, sizes, dst,
+                                                    _MAX_STATS, 1, 1, C.byref(h)), "frame_graph_create")
+        self._h = h
+        self._ready = torch.cuda.Event()
+
+    def launch(self, mesh_a, mesh_b, stream=None):
+        """Enqueue the frame for `mesh_a` / `mesh_b` (rigid moves of the
+        captured meshes' bases)."""
+        if (mesh_a._root, mesh_b._root) != self._roots:
+            raise ValueError("a FrameGraph replays moves of the meshes it was captured with")
+        g_ma, g_mb = mesh_a.device_view(), mesh_b.device_view()
+        _lib.check(_lib.lib().gd_frame_graph_launch(self._h, C.byref(g_ma), C.byref(g_mb),
+                                                    stream or _lib.stream_ptr()), "frame_graph_launch")
+        for bvh, m in zip(self.trees, (mesh_a, mesh_b)):
+            bvh._mesh = m  # the boxes now describe the moved mesh
+            bvh._export_cache = None
+            bvh._host_boxes = None
+        for p in self.plans:
+            p.meshes = (mesh_a, mesh_b)
+            p.g_ma, p.g_mb = g_ma, g_mb
+        self._ready.record()
+        return self
+
+    def results(self) -> dict:
+        """Wait for the launched frame; {kind: QueryResult}."""
+        self._ready.synchronize()
+        out = {}
+        for kind, p, buf in zip(self.kinds, self.plans, self._pinned):
+            base = buf.data_ptr()
+            r = _lib.GdResult.from_address(base)
+            stats = (_lib.GdIterStat * _MAX_STATS).from_address(base + C.sizeof(_lib.GdResult))
+            if r.pending and r.status == 0:  # a chunked traversal: the remaining rounds, synchronously
+                p._finish_rounds(r, _lib.stream_ptr())
+                out[kind] = _result(kind, p.res, p.stats)
+            else:
+                out[kind] = _result(kind, r, stats)
+        return out
+
+    def run(self, mesh_a, mesh_b) -> dict:
+        return self.launch(mesh_a, mesh_b).results()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.lib().gd_frame_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # recently used query plans of this host thread (a plan uses the thread's
 # workspace), keyed by (trees, config, kind, warm pair, device); the trees are
 # held weakly

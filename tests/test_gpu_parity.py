@@ -194,6 +194,43 @@ def test_rotation_frames_golden(md, gpu, golden_meta):
         assert d == rec["min"]["distance"] and pair == (rec["min"]["tri_a"], rec["min"]["tri_b"])
 
 
+def test_rotation_frames_golden_sequence_paths(md, gpu, golden_meta):
+    """The same golden config-3 frames through the sequence drivers: the
+    temporal warm start (run_sequence(warm=True): each frame seeded on the
+    device with the previous frame's witness), the pipelined and plain
+    loops, and the per-frame CUDA graph (run_sequence_minmax: refit A + refit B + min
+    + max replayed as one graph) -- all the reference's distances and
+    witnesses bit for bit."""
+    tz, tb = md.ring_pair_base(100, 50)
+    bvh_a, bvh_b = md.build_f12(tz), md.build_f12(tb)
+    recs = golden_meta["frames"]
+    xfs = [md.ring_frame_transforms(rec["frame"]) for rec in recs]
+    want = {q: np.array([[r[q]["distance"], r[q]["tri_a"], r[q]["tri_b"]] for r in recs]) for q in ("min", "max")}
+    for q in ("min", "max"):
+        for opts in ({"warm": True}, {"warm": True, "pipelined": False}, {}, {"graph": True}):
+            got = md.run_sequence(tz, tb, bvh_a, bvh_b, xfs, q, **opts)
+            np.testing.assert_array_equal(got, want[q], err_msg=f"{q} {opts}")
+    both = md.run_sequence_minmax(tz, tb, bvh_a, bvh_b, xfs)
+    for q in ("min", "max"):
+        np.testing.assert_array_equal(both[q], want[q], err_msg=q)
+    # a FrameGraph replayed frame by frame, then the plain API on the same trees
+    a0, b0 = md.apply_transform(tz, xfs[0][0]), md.apply_transform(tb, xfs[0][1])
+    fg = md.FrameGraph(a0, b0, bvh_a, bvh_b, ("max", "min"))
+    for rec, (xa, xb) in zip(recs, xfs):
+        a, b = md.apply_transform(tz, xa), md.apply_transform(tb, xb)
+        out = fg.run(a, b)
+        for q in ("min", "max"):
+            assert (out[q].distance, out[q].witness.tri_a, out[q].witness.tri_b) == (
+                rec[q]["distance"], rec[q]["tri_a"], rec[q]["tri_b"]), (rec["frame"], q)
+        assert out["min"].witness.point_a.shape == (3,)
+        # the trees now hold this frame's boxes: the plain query agrees
+        r = md.run_min_query(a, b, bvh_a, bvh_b)
+        assert r.distance == rec["min"]["distance"]
+    fg.close()
+    with pytest.raises(ValueError):
+        md.FrameGraph(a0, b0, bvh_a, bvh_b, ("median",))
+
+
 def test_brute_force_device(md, gpu, golden_meta):
     for rec in golden_meta["engine"][:10]:
         ma, mb = md.gen_scene(rec["kind"], rec["params"])
