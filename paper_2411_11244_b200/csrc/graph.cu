@@ -14,7 +14,7 @@
 namespace gd {
 
 void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s);
-const void* refit_kernel();
+bool is_refit_kernel(const void* f);
 void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done,
                  int round);
@@ -29,6 +29,9 @@ struct FrameGraph {
   GdBvh A{}, B{};
   GdMesh ma{}, mb{};
   std::vector<cudaGraphNode_t> refit_nodes, query_nodes;
+  std::vector<cudaKernelNodeParams> refit_params, query_params;  // captured launch configurations
+  std::vector<GdBvh> refit_trees;
+  std::vector<QArgs> query_args;
   long long kernels = 0;
 };
 
@@ -70,10 +73,15 @@ void* frame_graph_create(const GdMesh& ma, const GdMesh& mb, const GdBvh& A, con
       cudaKernelNodeParams p;
       GD_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
       ++fg->kernels;
-      if (p.func == refit_kernel())
+      if (is_refit_kernel(p.func)) {
         fg->refit_nodes.push_back(nd);
-      else if (is_query_kernel(p.func))
+        fg->refit_params.push_back(p);
+        fg->refit_trees.push_back(*static_cast<const GdBvh*>(p.kernelParams[0]));
+      } else if (is_query_kernel(p.func)) {
         fg->query_nodes.push_back(nd);
+        fg->query_params.push_back(p);
+        fg->query_args.push_back(*static_cast<const QArgs*>(p.kernelParams[0]));
+      }
     }
   } catch (...) {
     if (cap) {
@@ -97,25 +105,24 @@ void frame_graph_launch(void* h, const GdMesh& ma, const GdMesh& mb, cudaStream_
   GD_CHECK(current_device() == fg->dev, GD_ERR_INVALID, "frame graph launched on another device");
   GD_CHECK(ma.vtx == fg->ma.vtx && mb.vtx == fg->mb.vtx && ma.nv == fg->ma.nv && mb.nv == fg->mb.nv,
            GD_ERR_TOPOLOGY, "a frame graph replays the meshes it was captured with (same base vertices), moved");
-  for (cudaGraphNode_t nd : fg->refit_nodes) {
-    cudaKernelNodeParams p;
-    GD_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
-    GdBvh T = *static_cast<const GdBvh*>(p.kernelParams[0]);
-    XfF32 x = xf32_host(T.box == fg->A.box ? ma : mb);
+  const XfF32 xa = xf32_host(ma), xb = xf32_host(mb);
+  for (size_t i = 0; i < fg->refit_nodes.size(); ++i) {
+    cudaKernelNodeParams p = fg->refit_params[i];
+    GdBvh T = fg->refit_trees[i];
+    XfF32 x = T.box == fg->A.box ? xa : xb;
     void* args[] = {&T, &x};
     p.kernelParams = args;
     p.extra = nullptr;
-    GD_CUDA(cudaGraphExecKernelNodeSetParams(fg->exec, nd, &p));
+    GD_CUDA(cudaGraphExecKernelNodeSetParams(fg->exec, fg->refit_nodes[i], &p));
   }
-  for (cudaGraphNode_t nd : fg->query_nodes) {
-    cudaKernelNodeParams p;
-    GD_CUDA(cudaGraphKernelNodeGetParams(nd, &p));
-    QArgs q = *static_cast<const QArgs*>(p.kernelParams[0]);
+  for (size_t i = 0; i < fg->query_nodes.size(); ++i) {
+    cudaKernelNodeParams p = fg->query_params[i];
+    QArgs q = fg->query_args[i];
     retransform(q, ma, mb);
     void* args[] = {&q};
     p.kernelParams = args;
     p.extra = nullptr;
-    GD_CUDA(cudaGraphExecKernelNodeSetParams(fg->exec, nd, &p));
+    GD_CUDA(cudaGraphExecKernelNodeSetParams(fg->exec, fg->query_nodes[i], &p));
   }
   GD_CUDA(cudaGraphLaunch(fg->exec, s));
   count_launches(fg->kernels);

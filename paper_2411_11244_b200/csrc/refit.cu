@@ -189,6 +189,147 @@ __global__ __launch_bounds__(kFold) void k_refit(GdBvh T, XfF32 x) {
   }
 }
 
+// k_refit for full 256-leaf blocks (every tree of >= 256 leaves): the same
+// boxes as k_refit.  128 threads, two adjacent leaves each: the thread's six
+// plane loads are in flight together, it unions its two leaf boxes into
+// their parent in registers, and levels 2 - 6 fold inside each warp with
+// shuffles -- no block barrier until the four warp roots meet in warp 0 for
+// the last two levels; warp 0 alone then publishes the subtree root and, in
+// the last-arriving block of a group, folds the group (the other warps have
+// exited: they do not wait on the arrival counter).  Leaf pairs go to global memory as three 16-byte
+// stores (sibling slots are 16-byte aligned); every internal node is stored
+// by the lane holding it, consecutive nodes of a level from consecutive
+// holders.  (ncu: the 256-thread version was bound by its per-level block
+// barriers and one load round trip per thread, profiles/r2*_refit.)
+__device__ __forceinline__ Box leaf_box(const XfF32& x, const float4 a, const float4 b4, const float4 c) {
+  Box b;
+  const V3<float> v0 = xf_apply(x, make_float4(a.x, a.y, a.z, 0.f));
+  b.lo[0] = b.hi[0] = v0.x;
+  b.lo[1] = b.hi[1] = v0.y;
+  b.lo[2] = b.hi[2] = v0.z;
+  grow(b, xf_apply(x, make_float4(a.w, b4.x, b4.y, 0.f)));
+  grow(b, xf_apply(x, make_float4(b4.z, b4.w, c.x, 0.f)));
+  grow(b, xf_apply(x, make_float4(c.y, c.z, c.w, 0.f)));
+  return b;
+}
+
+__global__ __launch_bounds__(128) void k_refit256(GdBvh T, XfF32 x) {
+  constexpr int NB = kFold;  // leaves per block
+  __shared__ Box wroot[4];
+  __shared__ __align__(16) Box stage[kFold + kFold / 2];  // the cascade's ping-pong levels
+  const unsigned L = (unsigned)T.leaf_count, W = (L + 31) >> 5;
+  const unsigned rank0 = blockIdx.x * NB;
+  const unsigned l0 = rank0 + 2 * threadIdx.x;  // this thread's leaves l0, l0 + 1
+  const float4* p = reinterpret_cast<const float4*>(T.leaf_vtx);
+  const float4 a0 = __ldg(p + l0), a1 = __ldg(p + l0 + 1);
+  const float4 b0 = __ldg(p + L + l0), b1 = __ldg(p + L + l0 + 1);
+  const float4 c0 = __ldg(p + 2 * L + l0), c1 = __ldg(p + 2 * L + l0 + 1);
+  // the extras mask and rank base of the leaves' 32-leaf word, loaded with
+  // the planes: a leaf with extras waits one more round trip, not two
+  const unsigned mask = __ldg(T.leaf_x + (l0 >> 5)), rank_base = __ldg(T.leaf_x + W + (l0 >> 5));
+  // leaves with 5 - 6 distinct vertices (~20 % on the rings): both leaves'
+  // extra vertices are requested together, one round trip for the pair
+  const unsigned bit = l0 & 31;
+  const bool xe = (mask >> bit) & 1u, xo = (mask >> (bit + 1)) & 1u;
+  const unsigned re = rank_base + __popc(mask & ((1u << bit) - 1));
+  const float4* xv = reinterpret_cast<const float4*>(T.leaf_xvtx);
+  float4 ex0, ex1, ox0, ox1;
+  if (xe) {
+    ex0 = __ldg(xv + 2 * re);
+    ex1 = __ldg(xv + 2 * re + 1);
+  }
+  if (xo) {
+    const unsigned ro = re + (xe ? 1u : 0u);
+    ox0 = __ldg(xv + 2 * ro);
+    ox1 = __ldg(xv + 2 * ro + 1);
+  }
+  Box e = leaf_box(x, a0, b0, c0);
+  Box o = leaf_box(x, a1, b1, c1);
+  if (xe) {
+    grow(e, xf_apply(x, ex0));
+    grow(e, xf_apply(x, ex1));
+  }
+  if (xo) {
+    grow(o, xf_apply(x, ox0));
+    grow(o, xf_apply(x, ox1));
+  }
+  {  // the sibling leaf pair: slots L + l0, L + l0 + 1 (48 bytes, 16-byte aligned)
+    float4* d = reinterpret_cast<float4*>(T.box + ((unsigned long long)L + l0) * 6);
+    d[0] = make_float4(e.lo[0], e.lo[1], e.lo[2], e.hi[0]);
+    d[1] = make_float4(e.hi[1], e.hi[2], o.lo[0], o.lo[1]);
+    d[2] = make_float4(o.lo[2], o.hi[0], o.hi[1], o.hi[2]);
+  }
+  Box b = box_union(e, o);
+  int lv = T.depth;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // level 1 (the leaf pairs' parents): node rank (rank0 >> 1) + threadIdx.x
+  store_box(T.box, ((1ull << (lv - 1)) - 1) + (rank0 >> 1) + threadIdx.x, b);
+  // levels 2 - 6 inside the warp: after step u the lanes with lane % 2^(u-1)
+  // == 0 hold the level-u nodes of the warp's 64 leaves
+#pragma unroll
+  for (int u = 2; u <= 6; ++u) {
+    b = shfl_union(b, 1 << (u - 2), 0xffffffffu);
+    if ((lane & ((1 << (u - 1)) - 1)) == 0)
+      store_box(T.box, ((1ull << (lv - u)) - 1) + (rank0 >> u) + (threadIdx.x >> (u - 1)), b);
+  }
+  if (lane == 0) wroot[wid] = b;
+  __syncthreads();
+  if (wid != 0) return;  // warp 0 alone finishes the block: its top levels and the cascade
+  // levels 7, 8: the four warp roots (lanes 0 - 3)
+  b = wroot[lane & 3];
+#pragma unroll
+  for (int u = 7; u <= 8; ++u) {
+    b = shfl_union(b, 1 << (u - 7), 0xffffffffu);
+    if (lane < 4 && (lane & ((1 << (u - 6)) - 1)) == 0)
+      store_box(T.box, ((1ull << (lv - u)) - 1) + (rank0 >> u) + (lane >> (u - 6)), b);
+  }
+  lv -= 8;
+  unsigned rank = blockIdx.x;  // this block's subtree root (lane 0): node rank at level lv
+  unsigned* cnt = T.leaf_x + 2 * W + 1;
+  while (lv > 0) {
+    // group of sibling subtree roots folded by its last-arriving block (as in k_refit)
+    const int g = min(lv, 8);
+    const unsigned gsize = 1u << g, group = rank >> g, ngroups = (1u << lv) >> g;
+    int is_last = 0;
+    if (lane == 0) {
+      // the only box another block reads: the subtree root, stored by lane 0
+      // itself, then released by its arrival (acq_rel: the last arrival also
+      // acquires every earlier block's root -- the RMWs on the counter form
+      // a release sequence); no full fence
+      store_box(T.box, ((1ull << lv) - 1) + rank, b);
+      unsigned old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt + ngroups + group) : "memory");
+      is_last = old == gsize - 1;
+      if (is_last) cnt[ngroups + group] = 0;  // ready for the next refit
+    }
+    if (!__shfl_sync(0xffffffffu, is_last, 0)) return;
+    // the other lanes read the roots too: order their loads after lane 0's acquire
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    // the warp folds the group's roots level by level through shared memory
+    // (ping-pong buffers), each node stored by the lane that computes it
+    Box* src = stage;
+    Box* dst = stage + kFold;
+    for (unsigned i = lane; i < gsize; i += 32)
+      src[i] = load_box_cg(T.box, ((1ull << lv) - 1) + ((unsigned long long)group << g) + i);
+    __syncwarp();
+    for (int k = 1; k <= g; ++k) {
+      const unsigned n = gsize >> k;
+      for (unsigned i = lane; i < n; i += 32) {
+        const Box r = box_union(src[2 * i], src[2 * i + 1]);
+        dst[i] = r;
+        store_box(T.box, ((1ull << (lv - k)) - 1) + ((unsigned long long)group << (g - k)) + i, r);
+      }
+      __syncwarp();
+      Box* t = src;
+      src = dst;
+      dst = t;
+    }
+    b = src[0];
+    lv -= g;
+    rank = group;
+  }
+}
+
 // per-leaf distinct vertex sets (gdist.h leaf_vtx / leaf_x / leaf_xvtx) from
 // the leaf records and the staged vertices
 __global__ __launch_bounds__(256) void k_leaf_vtx(GdBvh T) {
@@ -249,7 +390,7 @@ void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CUDA(cudaGetLastError());
 }
 
-const void* refit_kernel() { return (const void*)k_refit; }  // frame graphs (graph.cu)
+bool is_refit_kernel(const void* f) { return f == (const void*)k_refit || f == (const void*)k_refit256; }  // graph.cu
 
 void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.m == T.n_tris, GD_ERR_TOPOLOGY,
@@ -258,7 +399,10 @@ void refit(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   const long long L = T.leaf_count;
   GD_CHECK(L < (1ll << 31), GD_ERR_INVALID, "tree too large for 32-bit leaf ranks");
   const int bs = (int)std::min<long long>(L, kFold);
-  k_refit<<<(unsigned)(L / bs), bs, 0, s>>>(T, xf32_host(m));
+  if (bs == kFold)
+    k_refit256<<<(unsigned)(L / bs), 128, 0, s>>>(T, xf32_host(m));
+  else
+    k_refit<<<(unsigned)(L / bs), bs, 0, s>>>(T, xf32_host(m));
   const long long launches = 1;
   GD_CUDA(cudaGetLastError());
   count_launches(launches);
