@@ -13,6 +13,9 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "engine.cuh"
@@ -245,8 +248,27 @@ size_t build_workspace_size(int64_t m, int64_t nv) {
   return std::max(build_layout(m).total, layout_ws(nv).total);
 }
 
+// GD_BUILD_TIMING=1: per-phase wall clock of bvh_build on stderr (stream
+// synchronised at each mark; scripts/exp_build.py)
+struct PhaseClock {
+  bool on;
+  cudaStream_t s;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseClock(cudaStream_t st) : on(std::getenv("GD_BUILD_TIMING") != nullptr), s(st) {
+    if (on) t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "  build %-22s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
 void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t* prim_order_host,
                int64_t* leaf_tris_host, cudaStream_t s) {
+  PhaseClock clk(s);
   const int64_t m = mesh.m;
   GD_CHECK(m >= 1, GD_ERR_INVALID, "cannot build a BVH over an empty mesh");
   GD_CHECK(m < (1ll << 31), GD_ERR_INVALID, "mesh too large for 32-bit triangle ids");
@@ -277,6 +299,7 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
   GD_CUDA(cub::DeviceRadixSort::SortPairs(base + w.cub, cub_bytes, codes_in, codes_out, ids_in, ids_out, (int)m, 0,
                                           63, s));
   GD_CUDA(cudaGetLastError());
+  clk.mark("bounds+morton+sort");
 
   std::vector<int32_t> order(m);
   GD_CUDA(cudaMemcpyAsync(order.data(), ids_out, m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -286,10 +309,12 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
     std::vector<double> sa_h(m - 1);
     GD_CUDA(cudaMemcpyAsync(sa_h.data(), sa, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
     GD_CUDA(cudaStreamSynchronize(s));
+    clk.mark("sa + D2H");
     pair_greedy(sa_h.data(), m, is_left.data());
   } else {
     GD_CUDA(cudaStreamSynchronize(s));
   }
+  clk.mark("pairing (host)");
   // leaf assembly in Morton order (bvh.py:168-181)
   std::vector<uint32_t> first(L + 1);
   int64_t rank = 0;
@@ -312,9 +337,12 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
   GD_CUDA(cudaMemcpyAsync(first_d, first.data(), (L + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
   k_leaf_rec<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(mesh, ids_out, first_d, L, reinterpret_cast<int4*>(T.leaf_rec));
   GD_CUDA(cudaGetLastError());
+  clk.mark("leaf assembly + records");
   bvh_layout(mesh, T, ws, ws_bytes, s);  // reuses the workspace (stream-ordered)
+  clk.mark("vertex layout + staging");
   refit(mesh, T, s);
   GD_CUDA(cudaStreamSynchronize(s));
+  clk.mark("refit");
 }
 
 }  // namespace gd

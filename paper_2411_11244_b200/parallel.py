@@ -119,22 +119,40 @@ def run_sequence_minmax(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kinds=("min", 
             w = r.witness
             local[k][f] = (r.distance, -1 if w is None else w.tri_a, -1 if w is None else w.tri_b)
 
-    graphs, pending = [], None
-    try:
-        for i, f in enumerate(mine):
-            a, b = moved(f)
-            if len(graphs) < 2:
-                graphs.append(FrameGraph(a, b, bvh_a, bvh_b, kinds, cfg))
-            g = graphs[i % 2].launch(a, b)
-            if pending is not None:
-                take(*pending)
-            pending = (f, g)
+    # the two graphs are kept for the next call on the same trees / meshes
+    key = (id(bvh_a), id(bvh_b), id(mesh_a._root), id(mesh_b._root), tuple(kinds), cfg)
+    ent = _FRAME_GRAPHS.get(key)
+    if ent is None or ent[0] is not bvh_a or ent[1] is not bvh_b:
+        if ent is not None:
+            for g in ent[2]:
+                g.close()
+        ent = (bvh_a, bvh_b, [])
+        _FRAME_GRAPHS.clear()  # one sequence's graphs at a time (each holds two query workspaces)
+        _FRAME_GRAPHS[key] = ent
+    graphs, pending = ent[2], None
+    for i, f in enumerate(mine):
+        a, b = moved(f)
+        if len(graphs) < 2:
+            graphs.append(FrameGraph(a, b, bvh_a, bvh_b, kinds, cfg))
+        g = graphs[i % 2].launch(a, b)
         if pending is not None:
             take(*pending)
-    finally:
-        for g in graphs:
-            g.close()
+        pending = (f, g)
+    if pending is not None:
+        take(*pending)
     return {k: gather_frames(len(transforms), local[k], group) for k in kinds}
+
+
+_FRAME_GRAPHS: dict = {}
+
+
+def release_frame_graphs():
+    """Destroy the cached frame graphs of run_sequence_minmax (and their
+    query workspaces)."""
+    for ent in _FRAME_GRAPHS.values():
+        for g in ent[2]:
+            g.close()
+    _FRAME_GRAPHS.clear()
 
 
 def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cfg=None, group=None,
