@@ -227,6 +227,12 @@ int gd_bvh_build(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspa
  * in place, stages the vertices.  workspace: GdBvhSizes.build_workspace_bytes.
  * gd_bvh_build does this itself.  Asynchronous. */
 int gd_bvh_layout(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspace_bytes, void* stream);
+/* How this thread's last gd_bvh_build paired the triangles
+ * (_pair_to_power_of_two, bvh.py:98-181): 0 = no merge needed (a power of two),
+ * 1 = on the device (the greedy's complete matching by scans + sort; exact
+ * because the reference's slack stayed positive, checked), 2 = the exact
+ * host restatement (a deferral was possible, or NaN surface areas). */
+int gd_build_pairing_mode(void);
 
 /* float32 copy of mesh->vtx (the base vertices, before mesh->rot/trans)
  * into bvh->vtx32 at the slots of bvh->vmap.  Needed once per base vertex

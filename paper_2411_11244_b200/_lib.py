@@ -137,6 +137,7 @@ _SIGNATURES = {
     "gd_bvh_sizes": (C.c_int, [C.c_int64, C.c_int64, C.POINTER(GdBvhSizes)]),
     "gd_bvh_build": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P, C.c_size_t, P, P, P]),
     "gd_bvh_layout": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P, C.c_size_t, P]),
+    "gd_build_pairing_mode": (C.c_int, []),
     "gd_stage_vertices": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P]),
     "gd_mesh_relative": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdMesh)]),
     "gd_refit": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdBvh), P]),

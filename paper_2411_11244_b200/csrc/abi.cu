@@ -19,6 +19,7 @@ void set_profiling(int on);
 int phase_ms(float* out, int n);
 
 size_t build_workspace_size(int64_t m, int64_t nv);
+int build_pairing_mode();
 void bvh_layout(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, cudaStream_t s);
 void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t* prim_order_host,
                int64_t* leaf_tris_host, cudaStream_t s);
@@ -135,6 +136,8 @@ int gd_bvh_build(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspa
     bvh_build(*mesh, *bvh, workspace, workspace_bytes, prim_order_host, leaf_tris_host, S(stream));
   });
 }
+
+int gd_build_pairing_mode(void) { return gd::build_pairing_mode(); }
 
 int gd_bvh_layout(const GdMesh* mesh, GdBvh* bvh, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {

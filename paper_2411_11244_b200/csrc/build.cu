@@ -3,14 +3,17 @@
 //   k_bounds       float64 min/max over ALL vertices (bvh.py:82-83)
 //   k_morton       centroid ((p0+p1)+p2)/3, 21-bit quantisation, 63-bit
 //                  interleave, x at bit 0 (bvh.py:58-95)
-//   radix sort     stable (code, id) sort == np.lexsort((ids, codes))
+//   radix sort     stable (code, id) sort == np.lexsort((ids, codes)),
+//                  the repo's own LSD sort (primitives.cuh, sort.cu)
 //   k_pair_sa      float64 surface area of Morton neighbours (bvh.py:117-120)
-//   pair_greedy    exact greedy on the host (pairing.cpp)
-//   k_leaf_rec     one 32-byte record per leaf (gdist.h)
+//   k_pair_*       the greedy power-of-two pairing on the device (scans +
+//                  sort, checked exact), else the exact greedy on the host
+//                  (pairing.cpp)
+//   leaf assembly  leaf ranks by scan, leaf_tris / prim_order, k_leaf_rec
+//                  (one 32-byte record per leaf, gdist.h)
 //   bvh_layout     staged-vertex numbering by first use in leaf order
 //                  (k_first_use + radix sort + k_rec_remap), staging
 // then refit() fills every box.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -19,6 +22,7 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "primitives.cuh"
 
 namespace gd {
 
@@ -161,28 +165,33 @@ __global__ __launch_bounds__(256) void k_rec_remap(int32_t* rec, long long L, co
   for (int c = 0; c < 6; ++c) rec[8 * l + c] = vmap[rec[8 * l + c]];
 }
 
-struct LayoutWs {
-  size_t first, first_out, ids, ids_out, cub, cub_bytes, total;
-};
 static size_t al(size_t x) { return (x + 255) / 256 * 256; }
+
+// bump allocator over a workspace (offsets only: sizing and carving share it)
+struct Carve {
+  size_t o = 0;
+  size_t take(size_t bytes) {
+    const size_t r = o;
+    o = al(o + bytes);
+    return r;
+  }
+};
+
+struct LayoutWs {
+  size_t first, first_out, ids, ids_out, ktmp, vtmp, sort, total;
+};
 static LayoutWs layout_ws(int64_t nv) {
   LayoutWs w;
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)std::max<int64_t>(nv, 1), 0, 32);
-  size_t o = 0;
-  w.first = o;
-  o = al(o + nv * sizeof(uint32_t));
-  w.first_out = o;
-  o = al(o + nv * sizeof(uint32_t));
-  w.ids = o;
-  o = al(o + nv * sizeof(int32_t));
-  w.ids_out = o;
-  o = al(o + nv * sizeof(int32_t));
-  w.cub = o;
-  w.cub_bytes = cub_bytes;
-  o = al(o + cub_bytes);
-  w.total = o;
+  Carve c;
+  const size_t n = (size_t)std::max<int64_t>(nv, 1);
+  w.first = c.take(n * sizeof(uint32_t));
+  w.first_out = c.take(n * sizeof(uint32_t));
+  w.ids = c.take(n * sizeof(int32_t));
+  w.ids_out = c.take(n * sizeof(int32_t));
+  w.ktmp = c.take(n * sizeof(uint32_t));
+  w.vtmp = c.take(n * sizeof(int32_t));
+  w.sort = c.take(radix_sort_ws_bytes((long long)n));
+  w.total = c.o;
   return w;
 }
 
@@ -201,9 +210,9 @@ void bvh_layout(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, cudaStr
   if (nv > 0) {
     k_first_init<<<gv, 256, 0, s>>>(first, ids, nv);
     k_first_use<<<gl, 256, 0, s>>>(T.leaf_rec, L, first);
-    size_t cub_bytes = w.cub_bytes;
-    GD_CUDA(cub::DeviceRadixSort::SortPairs(base + w.cub, cub_bytes, first, first_out, ids, ids_out, (int)nv, 0, 32,
-                                            s));
+    // stable: unused vertices (key 0xFFFFFFFF) keep their id order at the end
+    radix_sort_pairs(first, ids, reinterpret_cast<uint32_t*>(base + w.ktmp), reinterpret_cast<int32_t*>(base + w.vtmp),
+                     first_out, ids_out, nv, 32, base + w.sort, s);
     k_vmap<<<gv, 256, 0, s>>>(ids_out, nv, T.vmap);
     k_rec_remap<<<gl, 256, 0, s>>>(T.leaf_rec, L, T.vmap);
   }
@@ -213,34 +222,311 @@ void bvh_layout(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, cudaStr
 
 size_t layout_workspace_size(int64_t nv) { return layout_ws(nv).total; }
 
+// ---------------------------------------------------------------------------
+// Device restatement of _pair_to_power_of_two (bvh.py:98-181).
+//
+// Without its feasibility deferrals the reference is the sequential greedy
+// matching of a path by increasing key (surface area, index) -- every key is
+// distinct -- stopped after `need` merges.  The complete greedy matching of a
+// path has a local rule: a pair is taken iff no adjacent pair with a smaller
+// key is taken, so along a run of keys increasing away from a local minimum
+// the taken pairs alternate (the minimum, then every second one) and a local
+// maximum is taken iff neither neighbour is.  Two scans give every pair's
+// distance to the local minimum of its run (k_pair_*); the greedy takes the
+// matching's pairs in key order, so the reference's merges are the `need`
+// smallest keys of the matching (radix sort).  That holds exactly when the
+// reference never deferred, i.e. when its slack (sum over runs of unmerged
+// triangles of floor(len / 2), minus the merges still needed; it never
+// increases) stayed positive -- equivalently when the final slack is >= 1,
+// which the build checks on the device.  Otherwise (and for NaN keys, whose
+// heap order is Python's) the exact host restatement (pairing.cpp) runs.
+struct PairKeys {
+  const double* sa;
+  long long E;  // pairs (n - 1)
+  __device__ __forceinline__ bool less(long long i, long long j) const {
+    const double a = sa[i], b = sa[j];
+    return a < b || (a == b && i < j);
+  }
+  // the left neighbour's key is smaller: i continues a run rising from the left
+  __device__ __forceinline__ bool ls(long long i) const { return i > 0 && less(i - 1, i); }
+  __device__ __forceinline__ bool rs(long long i) const { return i + 1 < E && less(i + 1, i); }
+};
+// last j <= i where a rising run starts (no smaller left neighbour)
+struct RunStartIn {
+  PairKeys k;
+  __device__ __forceinline__ int operator()(long long i) const { return k.ls(i) ? -1 : (int)i; }
+};
+struct StoreInt {
+  int* a;
+  __device__ __forceinline__ void operator()(long long i, int v, int) const { a[i] = v; }
+};
+// first j >= i where a run falling to the right ends (scanned right to left)
+struct RunEndIn {
+  PairKeys k;
+  __device__ __forceinline__ int operator()(long long r) const {
+    const long long i = k.E - 1 - r;
+    return k.rs(i) ? (int)k.E : (int)i;
+  }
+};
+struct StoreIntRev {
+  int* a;
+  long long E;
+  __device__ __forceinline__ void operator()(long long r, int v, int) const { a[E - 1 - r] = v; }
+};
+
+__global__ __launch_bounds__(256) void k_pair_nan(const double* sa, long long E, unsigned long long* flags) {
+  const long long i = blockIdx.x * 256ll + threadIdx.x;
+  const bool bad = i < E && sa[i] != sa[i];
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1ull);
+}
+
+// matched[i]: the pair is in the complete greedy matching
+__global__ __launch_bounds__(256) void k_pair_match(PairKeys k, const int* S, const int* Eend, uint8_t* matched) {
+  const long long i = blockIdx.x * 256ll + threadIdx.x;
+  if (i >= k.E) return;
+  const bool l = k.ls(i), r = k.rs(i);
+  bool m;
+  if (!l && !r)
+    m = true;  // local minimum
+  else if (l && !r)
+    m = ((i - S[i]) & 1) == 0;
+  else if (!l && r)
+    m = ((Eend[i] - i) & 1) == 0;
+  else  // local maximum: taken iff neither neighbour is
+    m = ((i - 1 - S[i - 1]) & 1) != 0 && ((Eend[i + 1] - (i + 1)) & 1) != 0;
+  matched[i] = m ? 1 : 0;
+}
+
+struct MatchedIn {
+  const uint8_t* m;
+  __device__ __forceinline__ int operator()(long long i) const { return m[i]; }
+};
+// compaction of the matched pairs: (order-preserving key of sa, index)
+struct MatchedOut {
+  const uint8_t* m;
+  const double* sa;
+  unsigned long long* keys;
+  int32_t* idx;
+  unsigned long long* count;
+  long long E;
+  __device__ __forceinline__ void operator()(long long i, int inc, int v) const {
+    if (v) {
+      keys[inc - 1] = dkey(sa[i]);
+      idx[inc - 1] = (int32_t)i;
+    }
+    if (i == E - 1) *count = (unsigned long long)inc;
+  }
+};
+
+// argmin segment trees over the pairs (node v: the index of the smallest
+// (sa, index) key below it, -1 = none); leaves at size + i
+struct ArgminTree {
+  const double* sa;
+  int* t;
+  long long size;
+  __device__ __forceinline__ bool less(int a, int b) const {  // -1 = +infinity
+    if (a < 0) return false;
+    if (b < 0) return true;
+    return sa[a] < sa[b] || (sa[a] == sa[b] && a < b);
+  }
+  __device__ __forceinline__ int pick(int a, int b) const { return less(a, b) ? a : b; }
+  // nearest j < p (largest) holding a key smaller than p's
+  __device__ int prev_smaller(int p) const {
+    long long v = size + p;
+    while (v > 1) {
+      if ((v & 1) && less(t[v - 1], p)) {
+        v = v - 1;
+        while (v < size) v = less(t[2 * v + 1], p) ? 2 * v + 1 : 2 * v;
+        return (int)(v - size);
+      }
+      v >>= 1;
+    }
+    return -1;
+  }
+  // nearest j > p (smallest) holding a key smaller than p's
+  __device__ int next_smaller(int p) const {
+    long long v = size + p;
+    while (v > 1) {
+      if (!(v & 1) && less(t[v + 1], p)) {
+        v = v + 1;
+        while (v < size) v = less(t[2 * v], p) ? 2 * v : 2 * v + 1;
+        return (int)(v - size);
+      }
+      v >>= 1;
+    }
+    return -1;
+  }
+  // smallest key among pairs [l, r]
+  __device__ int argmin(long long l, long long r) const {
+    int best = -1;
+    for (long long a = l + size, b = r + size + 1; a < b; a >>= 1, b >>= 1) {
+      if (a & 1) best = pick(best, t[a++]);
+      if (b & 1) best = pick(best, t[--b]);
+    }
+    return best;
+  }
+};
+
+// leaves: every pair (tree A) or the matching's pairs only (tree B)
+__global__ __launch_bounds__(256) void k_tree_leaves(ArgminTree T, long long E, const uint8_t* only) {
+  const long long i = blockIdx.x * 256ll + threadIdx.x;
+  if (i >= T.size) return;
+  T.t[T.size + i] = (i < E && (!only || only[i])) ? (int)i : -1;
+}
+__global__ __launch_bounds__(256) void k_tree_level(ArgminTree T, long long lo, long long hi) {
+  const long long v = lo + blockIdx.x * 256ll + threadIdx.x;
+  if (v < hi) T.t[v] = T.pick(T.t[2 * v], T.t[2 * v + 1]);
+}
+static void build_tree(const ArgminTree& T, long long E, const uint8_t* only, cudaStream_t s) {
+  k_tree_leaves<<<(unsigned)((T.size + 255) / 256), 256, 0, s>>>(T, E, only);
+  for (long long lo = T.size / 2; lo >= 1; lo /= 2)
+    k_tree_level<<<(unsigned)((lo + 255) / 256), 256, 0, s>>>(T, lo, 2 * lo);
+}
+
+// Phase 1 (the greedy before its slack first reaches 0): the matching's pairs
+// are taken in key order; pair p is costly -- it lowers the slack -- when the
+// run of unmerged triangles around it at that moment has even length and p
+// sits at an odd offset.  That run is bounded by the nearest matching pairs
+// with smaller keys on either side (taken before p).
+__global__ __launch_bounds__(256) void k_pair_costly(ArgminTree B, const uint8_t* matched, long long E, long long n,
+                                                      uint8_t* costly) {
+  const long long p = blockIdx.x * 256ll + threadIdx.x;
+  if (p >= E) return;
+  if (!matched[p]) {
+    costly[p] = 0;
+    return;
+  }
+  const int q = B.prev_smaller((int)p), r = B.next_smaller((int)p);
+  const long long s = q >= 0 ? q + 2 : 0, e = r >= 0 ? r - 1 : n - 1;
+  costly[p] = (((e - s + 1) & 1) == 0 && ((p - s) & 1) == 1) ? 1 : 0;
+}
+
+// the slack after the r-th pick (key order) is slack0 - costly picks so far;
+// k* = the pick that brings it to 0 (the reference defers after it)
+struct CostlySortedIn {
+  const int32_t* sorted;
+  const uint8_t* costly;
+  __device__ __forceinline__ int operator()(long long r) const { return costly[sorted[r]]; }
+};
+struct SlackOut {
+  long long slack0;
+  unsigned long long* kstar;  // ~0 = never
+  __device__ __forceinline__ void operator()(long long r, int inc, int v) const {
+    if (v && slack0 - inc <= 0 && slack0 - (inc - v) > 0) *kstar = (unsigned long long)r;
+  }
+};
+__global__ __launch_bounds__(256) void k_pair_take(const int32_t* sorted_idx, long long count, uint8_t* is_left) {
+  const long long r = blockIdx.x * 256ll + threadIdx.x;
+  if (r < count) is_left[sorted_idx[r]] = 1;
+}
+
+// runs of unmerged triangles: the next merged position at or after t
+struct NextMergedIn {
+  const uint8_t* is_left;
+  long long n;
+  __device__ __forceinline__ int operator()(long long r) const {
+    const long long t = n - 1 - r;
+    const bool merged = is_left[t] || (t > 0 && is_left[t - 1]);
+    return merged ? (int)t : (int)n;
+  }
+};
+
+// Phase 2 (slack 0): runs evolve independently.  In an even run only pairs at
+// even offsets are feasible; they are disjoint, so all are taken.  In an odd
+// run every pair is feasible: the smallest key is taken, leaving an even part
+// (all its even offsets taken) and an odd part that repeats.  One thread per
+// run; the runs are disjoint.
+__global__ __launch_bounds__(256) void k_pair_phase2(ArgminTree A, const int* next_merged, long long n,
+                                                      uint8_t* is_left) {
+  const long long t = blockIdx.x * 256ll + threadIdx.x;
+  if (t >= n) return;
+  // run starts from the phase-1 state only (next_merged[t] == t: t merged),
+  // never from is_left, which the other runs' threads are writing
+  if (next_merged[t] == t || (t > 0 && next_merged[t - 1] != t - 1)) return;
+  long long lo = t, hi = (long long)next_merged[t] - 1;
+  auto take_even = [&](long long a, long long b) {  // all even offsets of [a, b]
+    for (long long i = a; i + 1 <= b; i += 2) is_left[i] = 1;
+  };
+  while (hi - lo + 1 >= 2) {
+    if (((hi - lo + 1) & 1) == 0) {
+      take_even(lo, hi);
+      break;
+    }
+    const long long i = A.argmin(lo, hi - 1);
+    is_left[i] = 1;
+    if (((i - lo) & 1) == 0) {  // left part even, right part odd
+      take_even(lo, i - 1);
+      lo = i + 2;
+    } else {
+      take_even(i + 2, hi);
+      hi = i - 1;
+    }
+  }
+}
+
+// leaf assembly (bvh.py:168-181): a leaf starts at every Morton rank that is
+// not the right half of a merged pair; its rank is the count of earlier
+// starts (scan)
+struct LeafStartIn {
+  const uint8_t* is_left;
+  __device__ __forceinline__ int operator()(long long t) const { return (t > 0 && is_left[t - 1]) ? 0 : 1; }
+};
+struct LeafOut {
+  const uint8_t* is_left;
+  const int32_t* order;
+  uint32_t* first;
+  long long* leaf_tris;
+  long long* prim;
+  long long n, L;
+  unsigned long long* err;
+  __device__ __forceinline__ void operator()(long long t, int inc, int v) const {
+    prim[t] = order[t];
+    if (!v) return;
+    const long long leaf = inc - 1;
+    if (leaf >= L) {  // a pairing that does not give 2^k leaves (checked by the host)
+      atomicOr(err, 1ull);
+      return;
+    }
+    first[leaf] = (uint32_t)t;
+    leaf_tris[2 * leaf] = order[t];
+    leaf_tris[2 * leaf + 1] = is_left[t] ? order[t + 1] : -1;
+    if (t == n - 1 || (t == n - 2 && is_left[t])) first[leaf + 1] = (uint32_t)n;
+  }
+};
+
 struct BuildWs {
-  size_t lohi, codes_in, codes_out, ids_in, ids_out, sa, first, cub, total, cub_bytes;
+  size_t lohi, codes_in, codes_out, codes_tmp, ids_in, ids_out, ids_tmp, sa, S, Eend, flag, costly, treeA, treeB,
+      leaf_tris, prim, first, counters, aggr, sort, total;
 };
 static BuildWs build_layout(int64_t m) {
   BuildWs w;
-  size_t cub_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (const unsigned long long*)nullptr,
-                                  (unsigned long long*)nullptr, (const int32_t*)nullptr, (int32_t*)nullptr,
-                                  (int)std::max<int64_t>(m, 1), 0, 63);
-  size_t o = 0;
-  w.lohi = o;
-  o = al(o + 6 * sizeof(unsigned long long));
-  w.codes_in = o;
-  o = al(o + m * sizeof(unsigned long long));
-  w.codes_out = o;
-  o = al(o + m * sizeof(unsigned long long));
-  w.ids_in = o;
-  o = al(o + m * sizeof(int32_t));
-  w.ids_out = o;
-  o = al(o + m * sizeof(int32_t));
-  w.sa = o;
-  o = al(o + m * sizeof(double));
-  w.first = o;
-  o = al(o + (m + 1) * sizeof(uint32_t));
-  w.cub = o;
-  w.cub_bytes = cub_bytes;
-  o = al(o + cub_bytes);
-  w.total = o;
+  Carve c;
+  const size_t n = (size_t)std::max<int64_t>(m, 1);
+  int64_t L = 1;
+  while (L * 2 <= (int64_t)n) L *= 2;
+  w.lohi = c.take(6 * sizeof(unsigned long long));
+  w.codes_in = c.take(n * sizeof(unsigned long long));
+  w.codes_out = c.take(n * sizeof(unsigned long long));
+  w.codes_tmp = c.take(n * sizeof(unsigned long long));
+  w.ids_in = c.take(n * sizeof(int32_t));
+  w.ids_out = c.take(n * sizeof(int32_t));
+  w.ids_tmp = c.take(n * sizeof(int32_t));
+  w.sa = c.take(n * sizeof(double));
+  w.S = c.take(n * sizeof(int));
+  w.Eend = c.take(n * sizeof(int));
+  w.flag = c.take(2 * n);  // matched, is_left
+  w.costly = c.take(n);
+  size_t tsz = 1;
+  while (tsz < n) tsz <<= 1;
+  w.treeA = c.take(2 * tsz * sizeof(int));
+  w.treeB = c.take(2 * tsz * sizeof(int));
+  w.leaf_tris = c.take(2 * (size_t)L * sizeof(long long));
+  w.prim = c.take(n * sizeof(long long));
+  w.first = c.take(((size_t)L + 1) * sizeof(uint32_t));
+  w.counters = c.take(8 * sizeof(unsigned long long));
+  w.aggr = c.take((size_t)scan_tiles((long long)n) * sizeof(long long));
+  w.sort = c.take(radix_sort_ws_bytes((long long)n));
+  w.total = c.o;
   return w;
 }
 
@@ -261,10 +547,15 @@ struct PhaseClock {
     if (!on) return;
     cudaStreamSynchronize(s);
     const auto n = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "  build %-22s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+    std::fprintf(stderr, "  build %-24s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
     t = n;
   }
 };
+
+// which pairing the last build used (gd_build_pairing_mode): 0 none needed,
+// 1 device, 2 host (a deferral was possible, or NaN keys)
+static thread_local int g_pairing_mode = 0;
+int build_pairing_mode() { return g_pairing_mode; }
 
 void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t* prim_order_host,
                int64_t* leaf_tris_host, cudaStream_t s) {
@@ -287,55 +578,114 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
   auto* lohi = reinterpret_cast<unsigned long long*>(base + w.lohi);
   auto* codes_in = reinterpret_cast<unsigned long long*>(base + w.codes_in);
   auto* codes_out = reinterpret_cast<unsigned long long*>(base + w.codes_out);
+  auto* codes_tmp = reinterpret_cast<unsigned long long*>(base + w.codes_tmp);
   auto* ids_in = reinterpret_cast<int32_t*>(base + w.ids_in);
   auto* ids_out = reinterpret_cast<int32_t*>(base + w.ids_out);
+  auto* ids_tmp = reinterpret_cast<int32_t*>(base + w.ids_tmp);
   auto* sa = reinterpret_cast<double*>(base + w.sa);
+  auto* S = reinterpret_cast<int*>(base + w.S);
+  auto* Eend = reinterpret_cast<int*>(base + w.Eend);
+  auto* matched = reinterpret_cast<uint8_t*>(base + w.flag);
+  uint8_t* is_left = matched + m;
+  auto* leaf_tris_d = reinterpret_cast<long long*>(base + w.leaf_tris);
+  auto* prim_d = reinterpret_cast<long long*>(base + w.prim);
+  auto* first_d = reinterpret_cast<uint32_t*>(base + w.first);
+  auto* counters = reinterpret_cast<unsigned long long*>(base + w.counters);
+  void* sort_ws = base + w.sort;
 
   k_bounds_init<<<1, 32, 0, s>>>(lohi);
   k_bounds<<<num_sms() * 4, 256, 0, s>>>(mesh, lohi);
   const unsigned g = (unsigned)((m + 255) / 256);
   k_morton<<<g, 256, 0, s>>>(mesh, lohi, codes_in, ids_in);
-  size_t cub_bytes = w.cub_bytes;
-  GD_CUDA(cub::DeviceRadixSort::SortPairs(base + w.cub, cub_bytes, codes_in, codes_out, ids_in, ids_out, (int)m, 0,
-                                          63, s));
+  // stable (code, id) order == np.lexsort((ids, codes)) (bvh.py:93-94)
+  radix_sort_pairs(codes_in, ids_in, codes_tmp, ids_tmp, codes_out, ids_out, m, 63, sort_ws, s);
   GD_CUDA(cudaGetLastError());
   clk.mark("bounds+morton+sort");
 
-  std::vector<int32_t> order(m);
-  GD_CUDA(cudaMemcpyAsync(order.data(), ids_out, m * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  std::vector<uint8_t> is_left(m, 0);
-  if (m > L) {
+  GD_CUDA(cudaMemsetAsync(is_left, 0, (size_t)m, s));
+  GD_CUDA(cudaMemsetAsync(counters, 0, 8 * sizeof(unsigned long long), s));
+  const int64_t need = m - L;
+  g_pairing_mode = 0;
+  if (need > 0) {
+    const long long E = m - 1;
+    const unsigned ge = (unsigned)((E + 255) / 256);
     k_pair_sa<<<g, 256, 0, s>>>(mesh, ids_out, m, sa);
-    std::vector<double> sa_h(m - 1);
-    GD_CUDA(cudaMemcpyAsync(sa_h.data(), sa, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+    k_pair_nan<<<ge, 256, 0, s>>>(sa, E, counters + 0);
+    const PairKeys pk{sa, E};
+    int* aggr_i = reinterpret_cast<int*>(base + w.aggr);
+    device_scan<int>(RunStartIn{pk}, StoreInt{S}, E, OpMax{}, -1, aggr_i, s);
+    device_scan<int>(RunEndIn{pk}, StoreIntRev{Eend, E}, E, OpMin{}, (int)E, aggr_i, s);
+    k_pair_match<<<ge, 256, 0, s>>>(pk, S, Eend, matched);
+    // the matching's pairs in index order, keyed by their surface area
+    device_scan<int>(MatchedIn{matched}, MatchedOut{matched, sa, codes_in, ids_in, counters + 1, E}, E, OpAdd{}, 0,
+                     aggr_i, s);
+    unsigned long long cnt[2];
+    GD_CUDA(cudaMemcpyAsync(cnt, counters, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     GD_CUDA(cudaStreamSynchronize(s));
-    clk.mark("sa + D2H");
-    pair_greedy(sa_h.data(), m, is_left.data());
-  } else {
-    GD_CUDA(cudaStreamSynchronize(s));
-  }
-  clk.mark("pairing (host)");
-  // leaf assembly in Morton order (bvh.py:168-181)
-  std::vector<uint32_t> first(L + 1);
-  int64_t rank = 0;
-  for (int64_t i = 0; i < m;) {
-    first[rank] = (uint32_t)i;
-    leaf_tris_host[2 * rank] = order[i];
-    if (is_left[i]) {
-      leaf_tris_host[2 * rank + 1] = order[i + 1];
-      i += 2;
-    } else {
-      leaf_tris_host[2 * rank + 1] = -1;
-      i += 1;
+    // GD_FORCE_HOST_PAIRING: the host greedy regardless (tests compare both)
+    bool device_ok = cnt[0] == 0 && std::getenv("GD_FORCE_HOST_PAIRING") == nullptr;
+    if (device_ok) {
+      const long long nm = (long long)cnt[1];
+      // the matching in key order: stable sort of the index-ordered pairs by sa
+      radix_sort_pairs(codes_in, ids_in, codes_tmp, ids_tmp, codes_out, S, nm, 64, sort_ws, s);
+      long long size = 1;
+      while (size < E) size <<= 1;
+      const ArgminTree TA{sa, reinterpret_cast<int*>(base + w.treeA), size};
+      const ArgminTree TB{sa, reinterpret_cast<int*>(base + w.treeB), size};
+      build_tree(TB, E, matched, s);
+      uint8_t* costly = reinterpret_cast<uint8_t*>(base + w.costly);
+      k_pair_costly<<<ge, 256, 0, s>>>(TB, matched, E, m, costly);
+      GD_CUDA(cudaMemsetAsync(counters + 4, 0xFF, sizeof(unsigned long long), s));
+      const long long slack0 = m / 2 - need;
+      const long long upto = std::min<long long>(need, nm);
+      device_scan<int>(CostlySortedIn{S, costly}, SlackOut{slack0, counters + 4}, upto, OpAdd{}, 0, aggr_i, s);
+      unsigned long long kstar = 0;
+      GD_CUDA(cudaMemcpyAsync(&kstar, counters + 4, sizeof kstar, cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+      if (kstar == ~0ull) {
+        // the slack never reached 0: the `need` smallest pairs of the matching
+        GD_CHECK(nm >= need, GD_ERR_INVALID, "internal: greedy matching smaller than the merges needed");
+        k_pair_take<<<(unsigned)((need + 255) / 256), 256, 0, s>>>(S, need, is_left);
+      } else {
+        k_pair_take<<<(unsigned)((kstar + 1 + 255) / 256), 256, 0, s>>>(S, (long long)kstar + 1, is_left);
+        build_tree(TA, E, nullptr, s);
+        device_scan<int>(NextMergedIn{is_left, m}, StoreIntRev{Eend, m}, m, OpMin{}, (int)m, aggr_i, s);
+        k_pair_phase2<<<g, 256, 0, s>>>(TA, Eend, m, is_left);
+      }
+      GD_CUDA(cudaGetLastError());
     }
-    ++rank;
+    if (device_ok) {
+      g_pairing_mode = 1;
+      count_launches(9);
+      clk.mark("pairing (device)");
+    } else {
+      // exact host restatement of the greedy with its deferrals
+      g_pairing_mode = 2;
+      std::vector<double> sa_h(m - 1);
+      GD_CUDA(cudaMemcpyAsync(sa_h.data(), sa, (m - 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+      std::vector<uint8_t> left(m, 0);
+      pair_greedy(sa_h.data(), m, left.data());
+      GD_CUDA(cudaMemcpyAsync(is_left, left.data(), (size_t)m, cudaMemcpyHostToDevice, s));
+      GD_CUDA(cudaStreamSynchronize(s));
+      clk.mark("pairing (host)");
+    }
   }
-  GD_CHECK(rank == L, GD_ERR_INVALID, "internal: pairing produced a wrong leaf count");
-  first[L] = (uint32_t)m;
-  for (int64_t i = 0; i < m; ++i) prim_order_host[i] = order[i];
-  auto* first_d = reinterpret_cast<uint32_t*>(base + w.first);
-  GD_CUDA(cudaMemcpyAsync(first_d, first.data(), (L + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+  // leaf assembly in Morton order (bvh.py:168-181), records, host copies
+  // (codes_in reused as the ids' order is ids_out)
+  device_scan<int>(LeafStartIn{is_left}, LeafOut{is_left, ids_out, first_d, leaf_tris_d, prim_d, m, L, counters + 3},
+                   m, OpAdd{}, 0, reinterpret_cast<int*>(base + w.aggr), s);
+  {
+    unsigned long long bad = 0;
+    uint32_t last = 0;
+    GD_CUDA(cudaMemcpyAsync(&bad, counters + 3, sizeof bad, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaMemcpyAsync(&last, first_d + L, sizeof last, cudaMemcpyDeviceToHost, s));
+    GD_CUDA(cudaStreamSynchronize(s));
+    GD_CHECK(bad == 0 && last == (uint32_t)m, GD_ERR_INVALID, "internal: pairing produced a wrong leaf count");
+  }
   k_leaf_rec<<<(unsigned)((L + 255) / 256), 256, 0, s>>>(mesh, ids_out, first_d, L, reinterpret_cast<int4*>(T.leaf_rec));
+  GD_CUDA(cudaMemcpyAsync(prim_order_host, prim_d, m * sizeof(long long), cudaMemcpyDeviceToHost, s));
+  GD_CUDA(cudaMemcpyAsync(leaf_tris_host, leaf_tris_d, 2 * L * sizeof(long long), cudaMemcpyDeviceToHost, s));
   GD_CUDA(cudaGetLastError());
   clk.mark("leaf assembly + records");
   bvh_layout(mesh, T, ws, ws_bytes, s);  // reuses the workspace (stream-ordered)
