@@ -638,16 +638,20 @@ void bvh_build(const GdMesh& mesh, GdBvh& T, void* ws, size_t ws_bytes, int64_t*
       GD_CUDA(cudaMemsetAsync(counters + 4, 0xFF, sizeof(unsigned long long), s));
       const long long slack0 = m / 2 - need;
       const long long upto = std::min<long long>(need, nm);
-      device_scan<int>(CostlySortedIn{S, costly}, SlackOut{slack0, counters + 4}, upto, OpAdd{}, 0, aggr_i, s);
-      unsigned long long kstar = 0;
-      GD_CUDA(cudaMemcpyAsync(&kstar, counters + 4, sizeof kstar, cudaMemcpyDeviceToHost, s));
-      GD_CUDA(cudaStreamSynchronize(s));
-      if (kstar == ~0ull) {
+      unsigned long long kstar = ~0ull;
+      if (slack0 > 0) {
+        device_scan<int>(CostlySortedIn{S, costly}, SlackOut{slack0, counters + 4}, upto, OpAdd{}, 0, aggr_i, s);
+        GD_CUDA(cudaMemcpyAsync(&kstar, counters + 4, sizeof kstar, cudaMemcpyDeviceToHost, s));
+        GD_CUDA(cudaStreamSynchronize(s));
+      }
+      const long long picks1 = slack0 <= 0 ? 0 : (kstar == ~0ull ? -1 : (long long)kstar + 1);  // -1: no zero slack
+      if (picks1 < 0) {
         // the slack never reached 0: the `need` smallest pairs of the matching
         GD_CHECK(nm >= need, GD_ERR_INVALID, "internal: greedy matching smaller than the merges needed");
         k_pair_take<<<(unsigned)((need + 255) / 256), 256, 0, s>>>(S, need, is_left);
       } else {
-        k_pair_take<<<(unsigned)((kstar + 1 + 255) / 256), 256, 0, s>>>(S, (long long)kstar + 1, is_left);
+        // phase 1 up to the pick that zeroes the slack (none if it starts at 0)
+        if (picks1 > 0) k_pair_take<<<(unsigned)((picks1 + 255) / 256), 256, 0, s>>>(S, picks1, is_left);
         build_tree(TA, E, nullptr, s);
         device_scan<int>(NextMergedIn{is_left, m}, StoreIntRev{Eend, m}, m, OpMin{}, (int)m, aggr_i, s);
         k_pair_phase2<<<g, 256, 0, s>>>(TA, Eend, m, is_left);

@@ -38,6 +38,17 @@ def test_build_matches_oracle_random(md, gpu, oracle, seed):
     assert modes <= {0, 1, 2}
 
 
+def test_build_matches_oracle_small_sizes(md, gpu, oracle):
+    """Every size 1 .. 80 (the pairing's slack starts at 0 for several,
+    e.g. 3, 5, 6, 7, 11): the device build equals the oracle's."""
+    for n in range(1, 81):
+        a, _ = md.gen_scene("random-blobs", {"n": n, "seed": n})
+        t = md.build_f12(a)
+        want = oracle.build_tree(a.vertices, a.triangles)
+        np.testing.assert_array_equal(t.prim_order, want.prim_order, err_msg=str(n))
+        np.testing.assert_array_equal(t.leaf_tris, want.leaf_tris, err_msg=str(n))
+
+
 def test_device_pairing_used_and_exact_on_tori(md, gpu, oracle):
     """Tori (sizes the reference pairs in seconds): the device pairing runs
     (mode 1) and equals the literal greedy."""

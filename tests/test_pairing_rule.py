@@ -52,9 +52,9 @@ def _rule(sa, n):
     slack0 = n // 2 - need
     cs = np.cumsum(costly[order])
     hit = np.flatnonzero(slack0 - cs[:need] <= 0)
-    if len(hit) == 0:
+    if slack0 > 0 and len(hit) == 0:
         return sorted(M[order[:need]].tolist())
-    k = hit[0]
+    k = hit[0] if slack0 > 0 else -1  # the slack may start at 0: no phase-1 pick at all
     is_left = np.zeros(n, bool); is_left[M[order[:k + 1]]] = True
     merged = is_left.copy(); merged[1:] |= is_left[:-1]
     um = ~merged
@@ -95,6 +95,16 @@ def test_two_phase_rule_equals_greedy(seed):
     else:  # all equal (one run rising with the index)
         sa = np.full(n - 1, 0.25)
     assert list(_rule(sa, n)) == list(oracle.greedy_pairs(sa, n)), (seed, n, kind)
+
+
+@pytest.mark.parametrize("n", range(3, 70))
+def test_two_phase_rule_small_n(n):
+    """Every small size, where the slack may start at 0 (n = 3, 5, 6, 7,
+    11, ...): random, tied and monotone keys."""
+    rng = np.random.default_rng(n)
+    for sa in (rng.random(n - 1), rng.integers(0, 2, n - 1).astype(np.float64), np.arange(n - 1, 0, -1.0),
+               np.full(n - 1, 1.0)):
+        assert list(_rule(sa, n)) == list(oracle.greedy_pairs(sa, n)), (n, sa)
 
 
 def test_two_phase_rule_on_torus_pairing():
