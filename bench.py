@@ -60,6 +60,7 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="a short run for ncu (no baselines)")
     ap.add_argument("--no-max", action="store_true", help="skip the max-query keys")
     ap.add_argument("--dry-run", action="store_true", help="launcher / collective plumbing only (no GPU work)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs (1, 4, 5)")
     return ap.parse_args()
 
 
@@ -234,6 +235,116 @@ def traverse_roofline(res, phases, bvh_a, bvh_b, kind):
             "traffic": traffic, "peak_source": src, "algorithmic_bytes": qb["expand_bytes"], "kernel_ms": expand_ms,
             "note": "algorithmic bytes (SURVEY 8d) count every box load; most hit L2 (traffic = ncu DRAM bytes "
                     "of one launch, profiles/kernel_traffic.json)"}
+
+
+def measure_query(md, _lib, a, b, ta, tb, kind, cfg, reps=5):
+    """One query of a config: median device ms over `reps` launches (CUDA
+    events; a chunked query -- several traversal rounds -- is timed through
+    its collect, host gaps between rounds included), the answer, and the
+    k_traverse roofline from a profiled run (single-round queries)."""
+    import ctypes as C
+
+    import torch
+
+    pq = md.PreparedQuery(a, b, ta, tb, cfg, kind)
+    r = pq.run()
+    rounds = int(pq.res.rounds)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ms = []
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        s.record()
+        pq.launch()
+        if rounds > 1:
+            pq.collect()
+        e.record()
+        torch.cuda.synchronize()
+        ms.append(s.elapsed_time(e))
+    if rounds == 1:
+        pq.collect()
+    out = {"query_ms": round(float(np.median(ms)), 6), "distance": r.distance,
+           "witness": [r.witness.tri_a, r.witness.tri_b] if r.witness else None, "rounds": rounds,
+           "expanded_pairs": r.expanded_pairs, "narrow_pairs": r.narrow_pairs, "band_pairs": r.band_pairs,
+           "peak_front": r.peak_front}
+    if rounds == 1:
+        L = _lib.lib()
+        L.gd_set_profiling(1)
+        pq.launch()
+        res = pq.collect()
+        ph = (C.c_float * 5)()
+        L.gd_query_phase_ms(ph, 5)
+        L.gd_set_profiling(0)
+        phases = {"init": ph[0], "expand": ph[1], "narrow": ph[2], "exact": ph[3], "final": ph[4]}
+        out["phases_ms"] = {k: round(v, 6) for k, v in phases.items()}
+        rl = traverse_roofline(res, phases, ta, tb, kind)
+        rl["traffic"] = None  # the committed ncu DRAM capture is of the rings workload only
+        out["roofline"] = rl
+    else:
+        out["roofline"] = None
+        out["roofline_note"] = "chunked traversal (the front outgrew the arena): per-round phases not timed"
+    return out
+
+
+def configs_section(md, _lib):
+    """BASELINE.json's other configs on this GPU (rank 0, N = 1), each
+    query with its own device time, answer and k_traverse roofline:
+    config 1 (tori 2 x 10K, min + max, with the unmodified reference on the
+    host cores: time and distance / witness parity), config 4 (nested
+    shells 2 x 2M, min + max; no front cap), config 5 (rings 100K -> 30M
+    total triangles, min + max; the 8-GPU split of config 5 needs the 8-GPU
+    box, see the split keys of an N > 1 run)."""
+    import torch
+
+    out = {}
+    t0 = time.perf_counter()
+    # config 1
+    a, b = md.gen_scene("interlocked-rings", {"nu": 100, "nv": 50})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    ref = load_reference()
+    c1 = {}
+    for kind in ("min", "max"):
+        rec = measure_query(md, _lib, a, b, ta, tb, kind, md.EngineConfig())
+        if ref is not None:
+            A, B = ref.TriangleMesh(a.vertices, a.triangles), ref.TriangleMesh(b.vertices, b.triangles)
+            RA, RB = ref.build_f12(A), ref.build_f12(B)
+            run = ref.run_min_query if kind == "min" else ref.run_max_query
+            times, rr = [], None
+            for _ in range(3):
+                t1 = time.perf_counter()
+                rr = run(A, B, RA, RB, ref.EngineConfig(threads=os.cpu_count() or 1))
+                times.append((time.perf_counter() - t1) * 1e3)
+            rec["reference"] = {"ms": round(min(times), 3), "threads": os.cpu_count(), "kind": "reference",
+                                "sample": "the whole config-1 query, unmodified reference package (baseline/_ref), "
+                                          "best of 3",
+                                "distance_equal": rr.distance == rec["distance"],
+                                "witness_equal": [rr.witness.tri_a, rr.witness.tri_b] == rec["witness"]}
+        c1[kind] = rec
+    out["config1_tori_2x10K"] = c1
+    # config 4
+    a, b = md.gen_scene("nested-shells", {"lat": 1001, "lon": 1000, "r_inner": 0.8, "r_outer": 0.81})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    cfg4 = md.EngineConfig(front_hard_cap=1 << 40)
+    out["config4_nested_shells_2x2M"] = {kind: measure_query(md, _lib, a, b, ta, tb, kind, cfg4, reps=3)
+                                         for kind in ("min", "max")}
+    del ta, tb
+    torch.cuda.empty_cache()
+    # config 5
+    c5 = {}
+    for nu, nv in [(250, 100), (500, 150), (1000, 250), (1500, 500), (2500, 1000), (5000, 1500)]:
+        tz, tbase = md.ring_pair_base(nu, nv)
+        A, B = md.build_f12(tz), md.build_f12(tbase)
+        xa, xb = md.ring_frame_transforms(0)
+        a, b = md.apply_transform(tz, xa), md.apply_transform(tbase, xb)
+        md.refit(A, a)
+        md.refit(B, b)
+        cfg = md.EngineConfig(front_hard_cap=1 << 28)
+        c5[f"{2 * tz.n_triangles}"] = {kind: measure_query(md, _lib, a, b, A, B, kind, cfg) for kind in ("min", "max")}
+        del A, B
+        torch.cuda.empty_cache()
+    out["config5_rings_sweep_total_tris"] = c5
+    out["wall_s"] = round(time.perf_counter() - t0, 2)
+    out["note"] = "device ms per query (CUDA events, median); rooflines as the headline's (k_traverse algorithmic bytes)"
+    return out
 
 
 def frame_graph_section(md, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_dev, seq):
@@ -890,6 +1001,14 @@ def main():
                 out["cpu_baseline"] = cpu_baseline(args, ctx, args.cpu_budget)
             except Exception as exc:  # report, never hide
                 out["cpu_baseline"] = {"value": None, "error": repr(exc)}
+        if not args.no_configs and not args.profile_only and world == 1:
+            try:
+                import paper_2411_11244_b200 as md
+                from paper_2411_11244_b200 import _lib
+
+                out["configs"] = configs_section(md, _lib)
+            except Exception as exc:  # report, never hide
+                out["configs"] = {"error": repr(exc)}
         print(json.dumps(out))
     if world > 1:
         import torch.distributed as dist

@@ -96,6 +96,7 @@ struct alignas(16) QState {
   GdIterStat stats[kMaxIters];       // contiguous device->host copy
   unsigned long long t_it[kMaxIters + 1];      // %globaltimer at iteration boundaries
   unsigned long long t_sweep[kMaxIters];       // last block's sweep end (profiling)
+  unsigned long long t_plan[kMaxIters + 1];    // block 0: next sweep planned after iteration i's barrier
 };
 
 

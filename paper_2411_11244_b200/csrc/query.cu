@@ -104,12 +104,16 @@ int phase_ms(float* out, int n) {
   if (g_last_state && n > 5) {
     // per iteration: total, then (n > 5 + iterations) the sweep part
     int iters = 0;
-    unsigned long long t[kMaxIters + 1], sw[kMaxIters];
+    unsigned long long t[kMaxIters + 1], sw[kMaxIters], pl[kMaxIters + 1];
     GD_CUDA(cudaMemcpy(&iters, &g_last_state->iter, sizeof(int), cudaMemcpyDeviceToHost));
     GD_CUDA(cudaMemcpy(t, g_last_state->t_it, sizeof(t), cudaMemcpyDeviceToHost));
     GD_CUDA(cudaMemcpy(sw, g_last_state->t_sweep, sizeof(sw), cudaMemcpyDeviceToHost));
+    GD_CUDA(cudaMemcpy(pl, g_last_state->t_plan, sizeof(pl), cudaMemcpyDeviceToHost));
     for (int i = 0; i < iters && k < n; ++i, ++k) out[k] = (float)((double)(t[i + 1] - t[i]) * 1e-6);
     for (int i = 0; i < iters && k < n; ++i, ++k) out[k] = (float)((double)(sw[i] > t[i] ? sw[i] - t[i] : 0) * 1e-6);
+    // then the planning after each barrier (commit + plan of the next sweep, block 0)
+    for (int i = 0; i < iters && k < n; ++i, ++k)
+      out[k] = (float)((double)(pl[i + 1] > t[i + 1] ? pl[i + 1] - t[i + 1] : 0) * 1e-6);
   }
   return k;
 }

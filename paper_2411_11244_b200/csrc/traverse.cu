@@ -935,6 +935,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
         else
           plan_sweep<kMax>(qs, t, nx, rec);
       }
+      if (rec && q.profile) S->t_plan[p.it + 1] = globaltimer_ns();
     }
     __syncthreads();
     b ^= 1;

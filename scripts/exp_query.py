@@ -37,8 +37,8 @@ def once(warm=None, reps=5):
     best = None
     for _ in range(reps):
         r = pq.run()
-        ph = (C.c_float * 64)()
-        n = L.gd_query_phase_ms(ph, 64)
+        ph = (C.c_float * 256)()
+        n = L.gd_query_phase_ms(ph, 256)
         vals = list(ph[:n])
         if best is None or sum(vals[:5]) < sum(best[:5]):
             best = vals
@@ -55,7 +55,9 @@ for warm in (None, "self"):
            "iters": [{"k": s.k, "in": s.front_in, "out": s.front_out, "culled": s.culled,
                       "bound": round(s.bound_after, 6), "ms": round(ph[5 + i], 4) if 5 + i < len(ph) else None,
                       "sweep_ms": round(ph[5 + len(r.iterations) + i], 4)
-                      if 5 + len(r.iterations) + i < len(ph) else None}
+                      if 5 + len(r.iterations) + i < len(ph) else None,
+                      "plan_ms": round(ph[5 + 2 * len(r.iterations) + i], 4)
+                      if 5 + 2 * len(r.iterations) + i < len(ph) else None}
                      for i, s in enumerate(r.iterations)],
            }
     print(json.dumps(out))
