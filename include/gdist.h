@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 13
+#define GDIST_ABI_VERSION 14
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -91,8 +91,13 @@ typedef struct GdBvhSizes {
  *              scale of the float32 transform's rounding, read by queries)
  *   leaf_xvtx: 2 * L float4 (capacity): the 5th and 6th distinct vertex
  *              (repeated when only five) of each masked leaf, by rank
- * leaf_vtx, leaf_x and leaf_xvtx are written by gd_stage_vertices; the
- * refit streams them. */
+ *   leaf_tri : L * 20 float32 = five float4 per leaf: the two triangles'
+ *              staged (base) vertices a0 a1 a2 b0 b1 b2 as 18 floats, then
+ *              the float bits of tri0, tri1 (a single-triangle leaf repeats
+ *              triangle 0 and has tri1 = -1): the narrow phase's one
+ *              contiguous load per leaf instead of a record + six gathers
+ * leaf_vtx, leaf_x, leaf_xvtx and leaf_tri are written by
+ * gd_stage_vertices; the refit streams the first three. */
 typedef struct GdBvh {
   float* box;
   int32_t* leaf_rec;
@@ -106,6 +111,7 @@ typedef struct GdBvh {
   int64_t nv;
   int32_t depth;
   int32_t _pad;
+  float* leaf_tri;
 } GdBvh;
 
 /* EngineConfig (query.py:51-102).  `threads` and `batch_size` have no device

@@ -65,6 +65,7 @@ class GdBvh(C.Structure):
         ("nv", C.c_int64),
         ("depth", C.c_int32),
         ("_pad", C.c_int32),
+        ("leaf_tri", C.c_void_p),
     ]
 
 

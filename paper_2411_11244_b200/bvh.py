@@ -57,7 +57,8 @@ class F12Bvh:
     traversal boxes, node i at slot i + 1), `_leaf_rec` (L x 8 int32 leaf
     records), `_vtx32` (float32 copy of the base vertices of `_staged`, in
     first-use order), `_vmap` (staged slot of each mesh vertex), and the
-    streamed per-leaf vertex sets `_leaf_vtx`, `_leaf_x`, `_leaf_xvtx`.
+    streamed per-leaf vertex sets `_leaf_vtx`, `_leaf_x`, `_leaf_xvtx`, and
+    `_leaf_tri` (both triangles of every leaf, for the narrow phase).
     Host state: `leaf_tris` (L, 2) int64, `prim_order` (m,) int64, `depth`.
     """
 
@@ -72,7 +73,7 @@ class F12Bvh:
         if node_min is not None:
             self._host_boxes = (np.asarray(node_min), np.asarray(node_max))
         self._box = self._leaf_rec = self._vtx32 = self._vmap = None
-        self._leaf_vtx = self._leaf_x = self._leaf_xvtx = None
+        self._leaf_vtx = self._leaf_x = self._leaf_xvtx = self._leaf_tri = None
         self._mesh = None            # mesh of the last device refit
         self._staged = None          # root mesh whose base vertices are in _vtx32
         self._layout_tris = None     # index buffer the leaf records were built from
@@ -160,6 +161,7 @@ class F12Bvh:
         self._leaf_x = _lib.torch().zeros(2 * ((L + 31) // 32) + 1 + 2 * (L >> 16) + 5, dtype=torch.int32,
                                           device=_lib.device())
         self._leaf_xvtx = _lib.empty(2 * L * 4, torch.float32)
+        self._leaf_tri = _lib.empty(L * 20, torch.float32)
 
     def device_view(self) -> _lib.GdBvh:
         """C view (include/gdist.h GdBvh), cached until a buffer changes."""
@@ -176,6 +178,7 @@ class F12Bvh:
         g.leaf_vtx = self._leaf_vtx.data_ptr()
         g.leaf_x = self._leaf_x.data_ptr()
         g.leaf_xvtx = self._leaf_xvtx.data_ptr()
+        g.leaf_tri = self._leaf_tri.data_ptr()
         g.leaf_count = self.leaf_count
         g.n_tris = len(self.prim_order)
         g.nv = nv

@@ -199,6 +199,46 @@ __device__ __forceinline__ Tri<float> leaf_tri32(const GdBvh& T, const XfF32& x,
   return i ? tri32(T, x, r.r0.w, r.r1.x, r.r1.y) : tri32(T, x, r.r0.x, r.r0.y, r.r0.z);
 }
 
+// both triangles of a leaf from leaf_tri (gdist.h): one 80-byte load,
+// transformed by xf_apply exactly as tri32 does (bitwise the same vertices)
+struct LeafTris {
+  Tri<float> t[2];
+  int tri0, tri1;
+  __device__ __forceinline__ int count() const { return tri1 >= 0 ? 2 : 1; }
+  __device__ __forceinline__ unsigned tri_id(int i) const { return (unsigned)(i ? tri1 : tri0); }
+};
+__device__ __forceinline__ LeafTris load_leaf_tris(const GdBvh& T, const XfF32& x, unsigned long long leaf) {
+  const float4* p = reinterpret_cast<const float4*>(T.leaf_tri) + 5 * leaf;
+  const float4 f0 = __ldg(p), f1 = __ldg(p + 1), f2 = __ldg(p + 2), f3 = __ldg(p + 3), f4 = __ldg(p + 4);
+  LeafTris r;
+  r.t[0].v[0] = xf_apply(x, make_float4(f0.x, f0.y, f0.z, 0.f));
+  r.t[0].v[1] = xf_apply(x, make_float4(f0.w, f1.x, f1.y, 0.f));
+  r.t[0].v[2] = xf_apply(x, make_float4(f1.z, f1.w, f2.x, 0.f));
+  r.t[1].v[0] = xf_apply(x, make_float4(f2.y, f2.z, f2.w, 0.f));
+  r.t[1].v[1] = xf_apply(x, make_float4(f3.x, f3.y, f3.z, 0.f));
+  r.t[1].v[2] = xf_apply(x, make_float4(f3.w, f4.x, f4.y, 0.f));
+  r.tri0 = __float_as_int(f4.z);
+  r.tri1 = __float_as_int(f4.w);
+  return r;
+}
+// one triangle (i = 0, 1) of a leaf: 40 bytes of the record
+__device__ __forceinline__ Tri<float> load_leaf_tri(const GdBvh& T, const XfF32& x, unsigned long long leaf, int i) {
+  const float4* p = reinterpret_cast<const float4*>(T.leaf_tri) + 5 * leaf;
+  Tri<float> t;
+  if (i == 0) {
+    const float4 f0 = __ldg(p), f1 = __ldg(p + 1), f2 = __ldg(p + 2);
+    t.v[0] = xf_apply(x, make_float4(f0.x, f0.y, f0.z, 0.f));
+    t.v[1] = xf_apply(x, make_float4(f0.w, f1.x, f1.y, 0.f));
+    t.v[2] = xf_apply(x, make_float4(f1.z, f1.w, f2.x, 0.f));
+  } else {
+    const float4 f2 = __ldg(p + 2), f3 = __ldg(p + 3), f4 = __ldg(p + 4);
+    t.v[0] = xf_apply(x, make_float4(f2.y, f2.z, f2.w, 0.f));
+    t.v[1] = xf_apply(x, make_float4(f3.x, f3.y, f3.z, 0.f));
+    t.v[2] = xf_apply(x, make_float4(f3.w, f4.x, f4.y, 0.f));
+  }
+  return t;
+}
+
 __device__ __forceinline__ Box tri_box(const Tri<float>& t) {
   Box b;
   b.lo[0] = fminf(fminf(t.v[0].x, t.v[1].x), t.v[2].x);

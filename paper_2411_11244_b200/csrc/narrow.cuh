@@ -121,13 +121,11 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
     const uint2 lp = i < n ? leaves[i] : make_uint2(0, 0);
     const float lkey = i < n ? keys[i] : 0.f;
     if (i < n && (!culling || survives<kMax>(lkey, ub2))) {
-      const LeafRec ra = load_leaf(q.A, lp.x), rb = load_leaf(q.B, lp.y);
+      // both leaves' triangles: one contiguous 80-byte load each (leaf_tri)
+      const LeafTris ra = load_leaf_tris(q.A, xa, lp.x), rb = load_leaf_tris(q.B, xb, lp.y);
       const int ca = ra.count(), cb = rb.count();
-      Tri<float> ta[2], tb[2];
-      ta[0] = leaf_tri32(q.A, xa, ra, 0);
-      tb[0] = leaf_tri32(q.B, xb, rb, 0);
-      if (ca > 1) ta[1] = leaf_tri32(q.A, xa, ra, 1);
-      if (cb > 1) tb[1] = leaf_tri32(q.B, xb, rb, 1);
+      const Tri<float>* ta = ra.t;
+      const Tri<float>* tb = rb.t;
       // per-triangle quantities once, not per pair
       Box ba[2], bb[2];
       V3<float> sa[2], sb[2];  // vertex sums (3 x centroid)
@@ -274,13 +272,15 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
     if (j < n) {
       ++tested;
       const uint2 c = cand[j];
-      const LeafRec ra = load_leaf(q.A, c.x >> 1), rb = load_leaf(q.B, c.y >> 1);
       const int ia = c.x & 1, ib = c.y & 1;
-      const Tri<float> A = leaf_tri32(q.A, xa, ra, ia), B = leaf_tri32(q.B, xb, rb, ib);
+      const Tri<float> A = load_leaf_tri(q.A, xa, c.x >> 1, ia), B = load_leaf_tri(q.B, xb, c.y >> 1, ib);
+      const float4* pa = reinterpret_cast<const float4*>(q.A.leaf_tri) + 5 * (unsigned long long)(c.x >> 1) + 4;
+      const float4* pb = reinterpret_cast<const float4*>(q.B.leaf_tri) + 5 * (unsigned long long)(c.y >> 1) + 4;
       d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
                : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
       upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
-      ids = make_uint2(ra.tri_id(ia), rb.tri_id(ib));
+      const float4 fa = __ldg(pa), fb = __ldg(pb);  // (the 5th word: tri ids; already in L1)
+      ids = make_uint2((unsigned)__float_as_int(ia ? fa.w : fa.z), (unsigned)__float_as_int(ib ? fb.w : fb.z));
     }
     // band: within E of the bound, and within E of the warp's best float32
     // distance (fbest is at least as good; k_refine drops the rest anyway)

@@ -376,9 +376,26 @@ __global__ __launch_bounds__(256) void k_leaf_vtx(GdBvh T) {
   }
 }
 
+// both triangles of every leaf as five float4 (gdist.h leaf_tri): the staged
+// base vertices a0 a1 a2 b0 b1 b2, then tri0 / tri1 as float bits
+__global__ __launch_bounds__(256) void k_leaf_tri(GdBvh T) {
+  const long long l = blockIdx.x * 256ll + threadIdx.x;
+  if (l >= T.leaf_count) return;
+  const LeafRec r = load_leaf(T, l);
+  const float4* v = reinterpret_cast<const float4*>(T.vtx32);
+  const float4 a0 = v[r.r0.x], a1 = v[r.r0.y], a2 = v[r.r0.z], b0 = v[r.r0.w], b1 = v[r.r1.x], b2 = v[r.r1.y];
+  float4* o = reinterpret_cast<float4*>(T.leaf_tri) + 5 * l;
+  o[0] = make_float4(a0.x, a0.y, a0.z, a1.x);
+  o[1] = make_float4(a1.y, a1.z, a2.x, a2.y);
+  o[2] = make_float4(a2.z, b0.x, b0.y, b0.z);
+  o[3] = make_float4(b1.x, b1.y, b1.z, b2.x);
+  o[4] = make_float4(b2.y, b2.z, __int_as_float(r.r1.z), __int_as_float(r.r1.w));
+}
+
 void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
   GD_CHECK(m.nv == T.nv, GD_ERR_TOPOLOGY, "mesh vertex count differs from the tree's");
-  GD_CHECK(T.leaf_vtx && T.leaf_x && T.leaf_xvtx, GD_ERR_INVALID, "GdBvh leaf vertex sets must be allocated");
+  GD_CHECK(T.leaf_vtx && T.leaf_x && T.leaf_xvtx && T.leaf_tri, GD_ERR_INVALID,
+           "GdBvh leaf vertex sets must be allocated");
   const long long W = (T.leaf_count + 31) / 32;
   // extras counter + the refit's cascade counters + the staging magnitude
   // (gdist.h leaf_x)
@@ -387,6 +404,7 @@ void stage_vertices(const GdMesh& m, const GdBvh& T, cudaStream_t s) {
     k_stage<<<(unsigned)((m.nv + 255) / 256), 256, 0, s>>>(m, T.vmap, reinterpret_cast<float4*>(T.vtx32),
                                                            T.leaf_x + stage_mag_slot(T.leaf_count));
   k_leaf_vtx<<<(unsigned)((T.leaf_count + 255) / 256), 256, 0, s>>>(T);
+  k_leaf_tri<<<(unsigned)((T.leaf_count + 255) / 256), 256, 0, s>>>(T);
   GD_CUDA(cudaGetLastError());
 }
 
