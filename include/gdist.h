@@ -379,7 +379,9 @@ int gd_tri_tri_batch(int kind, int precision, const void* t1, const void* t2, in
                      void* p, void* q, void* stream);
 
 /* Fast float32 narrow phase used by the traversal (FMA-contracted): d only.
- * t1, t2 float (n, 3, 3), d float (n).  For error-bound tests. */
+ * kind 0 = min, 1 = max, 2 = the min distance's conditioning-aware lower
+ * bound the exact band windows on.  t1, t2 float
+ * (n, 3, 3), d float (n).  For error-bound tests. */
 int gd_tri_tri_fast(int kind, const float* t1, const float* t2, int64_t n, float* d, void* stream);
 
 /* batch_min_lower / batch_max_upper / batch_enhanced_min_upper /

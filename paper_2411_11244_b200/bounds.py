@@ -153,7 +153,8 @@ def tri_tri_max(t1, t2):
 
 def tri_tri_fast(kind: str, t1, t2) -> np.ndarray:
     """The traversal's float32 (FMA-contracted) narrow phase, distances only;
-    exposed for the error-bound tests."""
+    exposed for the error-bound tests.  kind "min-lb": the conditioning-aware
+    lower bound of the float32 min distance that the exact band windows on."""
     a = np.ascontiguousarray(np.asarray(t1, dtype=np.float32).reshape(-1, 3, 3))
     b = np.ascontiguousarray(np.asarray(t2, dtype=np.float32).reshape(-1, 3, 3))
     n = len(a)
@@ -161,6 +162,7 @@ def tri_tri_fast(kind: str, t1, t2) -> np.ndarray:
     dev = _lib.device()
     ta, tb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
     d = torch.empty(n, dtype=torch.float32, device=dev)
-    _lib.check(_lib.lib().gd_tri_tri_fast(1 if kind == "max" else 0, _lib.ptr(ta), _lib.ptr(tb), n, _lib.ptr(d),
+    _lib.check(_lib.lib().gd_tri_tri_fast({"min": 0, "max": 1, "min-lb": 2}[kind], _lib.ptr(ta), _lib.ptr(tb), n,
+                                          _lib.ptr(d),
                                           _lib.stream_ptr()), "tri_tri_fast")
     return d.cpu().numpy()

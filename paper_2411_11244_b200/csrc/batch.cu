@@ -221,9 +221,23 @@ void tri_tri_batch(int kind, int precision, const void* t1, const void* t2, int6
   GD_CUDA(cudaGetLastError());
 }
 
+// the conditioning-aware lower bound of the float32 min distance
+// (geometry.cuh tri_tri_min_fast_lb): kind 2 of gd_tri_tri_fast
+__global__ void k_tri_tri_fast_lb(const float* t1, const float* t2, long long n, float* d) {
+  const long long i = blockIdx.x * 256ll + threadIdx.x;
+  if (i >= n) return;
+  Tri<float> a = load_tri_aos(t1, i), b = load_tri_aos(t2, i);
+  float dd, lb;
+  tri_tri_min_fast_lb(a, b, dd, lb);
+  d[i] = lb;
+}
+
 void tri_tri_fast(int kind, const float* t1, const float* t2, int64_t n, float* d, cudaStream_t s) {
+  GD_CHECK(kind >= 0 && kind <= 2, GD_ERR_INVALID, "kind must be 0 (min), 1 (max) or 2 (min lower bound)");
   if (n <= 0) return;
-  if (kind)
+  if (kind == 2)
+    k_tri_tri_fast_lb<<<blocks_for(n), 256, 0, s>>>(t1, t2, n, d);
+  else if (kind)
     k_tri_tri_fast<true><<<blocks_for(n), 256, 0, s>>>(t1, t2, n, d);
   else
     k_tri_tri_fast<false><<<blocks_for(n), 256, 0, s>>>(t1, t2, n, d);

@@ -66,15 +66,18 @@ __device__ __forceinline__ void dfs_leaf(const QArgs& q, unsigned ta, const Tri<
   const LeafRec r = load_leaf(q.B, leaf);
   for (int i = 0; i < r.count(); ++i) {
     const Tri<float> B = leaf_tri32(q.B, q.xb, r, i);
-    const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
-                         : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+    float d, lb;
+    if (kMax)
+      d = lb = sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+    else
+      tri_tri_min_fast_lb(A, B, d, lb);  // the band windows on the lower bound
     ++tested;
     const float ub = load_bound(S);
-    if (kMax ? d + E < ub : d - E > ub) continue;  // cannot be the answer
+    if (kMax ? d + E < ub : lb - E > ub) continue;  // cannot be the answer
     const unsigned long long slot = atomicAdd(&S->n_band, 1ull);
     if (slot < q.band_cap) {
       q.band_ids[slot] = make_uint2(ta, r.tri_id(i));
-      q.band_d[slot] = d;
+      q.band_d[slot] = lb;
     } else {
       S->band_overflow = 1;
     }

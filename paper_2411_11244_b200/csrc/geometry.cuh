@@ -140,6 +140,120 @@ __device__ __forceinline__ T tri_tri_min_d2(const Tri<T>& t1, const Tri<T>& t2, 
   return best;
 }
 
+// ---------------------------------------------------------------------------
+// float32 filter with a conditioning-aware LOWER BOUND.
+// A float32 closest-point pair always lies on the triangles (up to rounding),
+// so a float32 feature distance never UNDERestimates by more than a few ulps;
+// but it can OVERestimate when the closest points are ill-conditioned: the
+// Lumelsky solve of nearly parallel edges (its 2x2 determinant is
+// |u|^2 |v|^2 sin^2 theta) and the barycentric solve of a point over a thin or
+// distant triangle.  Measured on adversarial pairs (scripts/exp_narrow_error.py):
+// up to ~290 float32 ulps of the coordinate scale for near-contact pairs,
+// beyond the exact band's E / 2 = 128.  Each feature therefore also gets a
+// first-order bound D of the displacement of its computed closest point; the
+// distance excess along the (convex) feature profile is at most D when the
+// distance is below 2 D, else D^2 / (2 (d - D)).  lb = min over features of
+// (d - excess) (0 when a pierce is found) is what the exact band admits and
+// k_refine windows on; d itself still feeds the bound and f_best.
+constexpr float kU32 = 0x1p-24f;  // float32 unit roundoff
+
+__device__ __forceinline__ float feature_excess(float d, float disp) {
+  return d > 2.f * disp ? disp * disp / (2.f * (d - disp)) : disp;
+}
+
+// Lumelsky (segment_pair) in float32 + the displacement bound of its result
+__device__ __forceinline__ void segment_pair_lb(V3<float> p0, V3<float> u, V3<float> q0, V3<float> v,
+                                                V3<float>& p, V3<float>& q, float& disp) {
+  using A = Fast<float>;
+  V3<float> w = vsub<A>(q0, p0);
+  const float uu = vdot<A>(u, u), vv = vdot<A>(v, v), uv = vdot<A>(u, v);
+  const float uw = vdot<A>(u, w), vw = vdot<A>(v, w);
+  const float num = uw * vv - vw * uv, den = uu * vv - uv * uv;
+  float t = clamp_ratio<A>(num, den);
+  const float s = clamp_ratio<A>(t * uv - vw, vv);
+  t = clamp_ratio<A>(s * uv + uw, uu);
+  p = vmadd<A>(p0, t, u);
+  q = vmadd<A>(q0, s, v);
+  // first-step parameter error: dot products carry <= 3 u |.||.|, the
+  // differences of products <= 2 u more; x2 safety (16 u below)
+  if (!(uu > 0.f && vv > 0.f)) {  // a point: the projections are 1D, well conditioned
+    disp = 0.f;
+    return;
+  }
+  const float lu = sqrtf(uu), lv = sqrtf(vv), lw = sqrtf(vdot<A>(w, w));
+  const float dden = 16.f * kU32 * uu * vv;
+  const float dnum = 16.f * kU32 * lw * (lu * vv + lv * fabsf(uv));
+  float dt = 1.f;
+  if (den > dden) dt = fminf(1.f, (dnum + fabsf(num) / den * dden) / (den - dden));
+  const float sin2 = fminf(1.f, (den + dden) / (uu * vv));
+  // (both computed points lie on their segments: never more than |u| + |v|)
+  disp = fminf(2.f * dt * fmaxf(lu, lv) * sqrtf(fmaxf(sin2, 0.f)), lu + lv);
+}
+
+// point_triangle in float32 + the displacement bound of the closest point
+__device__ __forceinline__ V3<float> point_triangle_lb(V3<float> p, V3<float> a, V3<float> b, V3<float> c,
+                                                       float& disp) {
+  using A = Fast<float>;
+  const V3<float> q = point_triangle<A>(p, a, b, c);
+  const V3<float> ab = vsub<A>(b, a), ac = vsub<A>(c, a), bc = vsub<A>(c, b);
+  const V3<float> ap = vsub<A>(p, a), bp = vsub<A>(p, b), cp = vsub<A>(p, c);
+  const float L = sqrtf(fmaxf(fmaxf(vdot<A>(ab, ab), vdot<A>(ac, ac)), vdot<A>(bc, bc)));
+  const float R = sqrtf(fmaxf(fmaxf(vdot<A>(ap, ap), vdot<A>(bp, bp)), vdot<A>(cp, cp)));
+  const V3<float> n = vcross<A>(ab, ac);
+  const float tot = vdot<A>(n, n);                   // |ab x ac|^2, the solve's determinant
+  const float dtot = 64.f * kU32 * L * L * R * R;    // its error as computed from the d_i products
+  // barycentric error (x2 safety) times the edge length -- but the computed
+  // point lies on the triangle in every region (interior barycentrics are
+  // positive ratios of a common sum, edges / vertices are clamped), so it is
+  // never farther than the triangle's diameter L from the true closest point
+  disp = tot > 2.f * dtot ? fminf(2.f * 2.f * 32.f * kU32 * L * L * R * R / (tot - dtot) * L, L) : L;
+  return q;
+}
+
+__device__ __forceinline__ void tri_tri_min_fast_lb(const Tri<float>& t1, const Tri<float>& t2, float& d,
+                                                    float& lb) {
+  using A = Fast<float>;
+  float best = INFINITY, blb = INFINITY;
+  auto offer = [&](V3<float> p, V3<float> q, float disp) {
+    const V3<float> w = vsub<A>(p, q);
+    const float d2 = vdot<A>(w, w), df = sqrtf(d2);
+    best = fminf(best, d2);
+    blb = fminf(blb, df - feature_excess(df, disp));
+  };
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const V3<float> pa = t1.v[i], ua = vsub<A>(t1.v[(i + 1) % 3], pa);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const V3<float> qb = t2.v[j], vb = vsub<A>(t2.v[(j + 1) % 3], qb);
+      V3<float> p, q;
+      float disp;
+      segment_pair_lb(pa, ua, qb, vb, p, q, disp);
+      offer(p, q, disp);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    float disp;
+    V3<float> q = point_triangle_lb(t1.v[i], t2.v[0], t2.v[1], t2.v[2], disp);
+    offer(t1.v[i], q, disp);
+    q = point_triangle_lb(t2.v[i], t1.v[0], t1.v[1], t1.v[2], disp);
+    offer(q, t2.v[i], disp);
+  }
+  if (best > 0.f) {
+    bool hit = false;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      V3<float> x;
+      hit = hit || pierce<A>(t1.v[i], t1.v[(i + 1) % 3], t2.v[0], t2.v[1], t2.v[2], x);
+      hit = hit || pierce<A>(t2.v[i], t2.v[(i + 1) % 3], t1.v[0], t1.v[1], t1.v[2], x);
+    }
+    if (hit) best = 0.f;
+  }
+  d = sqrtf(best);
+  lb = best == 0.f ? 0.f : fmaxf(fminf(blb, d), 0.f);
+}
+
 // The same minimum distance^2 without witness points, features evaluated one
 // at a time (no unrolling): a fraction of the registers, so many more warps
 // per SM hide the float64 latency of the exact pass.  The minimum over the

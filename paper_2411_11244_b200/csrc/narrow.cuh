@@ -147,14 +147,18 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
           if (!kMax && culling && keep) keep = !axis_separated(ta[ia], tb[ib], sa[ia], sb[ib], ub2);
           if (!keep) continue;
           if (kMax || kRescan) {
-            const float d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr))
-                                 : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr));
+            float d, lb;
+            if (kMax)
+              d = lb = sqrtf(tri_tri_max_d2<Fast<float>, float, false>(ta[ia], tb[ib], nullptr, nullptr));
+            else
+              tri_tri_min_fast_lb(ta[ia], tb[ib], d, lb);
             if (kMax) upd = fmaxf(upd, d);
             ++tested;
             if (kRescan) {
-              // within E of the best float32 distance (k_refine's window), the
-              // thread keeps its best exact key; one atomic per warp below
-              if (kMax ? (d >= fb_rescan - E) : (d <= fb_rescan + E)) {
+              // within E of the best float32 distance (k_refine's window, on
+              // the conditioning-aware lower bound), the thread keeps its best
+              // exact key; one atomic per warp below
+              if (kMax ? (d >= fb_rescan - E) : (lb <= fb_rescan + E)) {
                 const Key128 k = exact_key<kMax>(q, ra.tri_id(ia), rb.tri_id(ib));
                 if (key_less(k, rbest)) rbest = k;
               }
@@ -267,7 +271,7 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   // warp-uniform loop (the band append below is warp-aggregated)
   for (unsigned long long base = blockIdx.x * 256ull; base < n; base += gridDim.x * 256ull) {
     const unsigned long long j = base + threadIdx.x;
-    float d = kMax ? -1.f : INFINITY;
+    float d = kMax ? -1.f : INFINITY, lb = d;
     uint2 ids = make_uint2(0, 0);
     if (j < n) {
       ++tested;
@@ -276,8 +280,11 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
       const Tri<float> A = load_leaf_tri(q.A, xa, c.x >> 1, ia), B = load_leaf_tri(q.B, xb, c.y >> 1, ib);
       const float4* pa = reinterpret_cast<const float4*>(q.A.leaf_tri) + 5 * (unsigned long long)(c.x >> 1) + 4;
       const float4* pb = reinterpret_cast<const float4*>(q.B.leaf_tri) + 5 * (unsigned long long)(c.y >> 1) + 4;
-      d = kMax ? sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr))
-               : sqrtf(tri_tri_min_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+      if (kMax) {
+        d = lb = sqrtf(tri_tri_max_d2<Fast<float>, float, false>(A, B, nullptr, nullptr));
+      } else {
+        tri_tri_min_fast_lb(A, B, d, lb);  // d: the float32 estimate; lb: what the band windows on
+      }
       upd = kMax ? fmaxf(upd, d) : fminf(upd, d);
       const float4 fa = __ldg(pa), fb = __ldg(pb);  // (the 5th word: tri ids; already in L1)
       ids = make_uint2((unsigned)__float_as_int(ia ? fa.w : fa.z), (unsigned)__float_as_int(ib ? fb.w : fb.z));
@@ -286,7 +293,7 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
     // distance (fbest is at least as good; k_refine drops the rest anyway)
     const float ub = load_bound(S);
     const float wu = kMax ? warp_max(upd) : warp_min(upd);  // every lane: a full-warp shuffle
-    const bool app = j < n && (kMax ? d >= fmaxf(ub, wu) - E : d <= fminf(ub, wu) + E);
+    const bool app = j < n && (kMax ? d >= fmaxf(ub, wu) - E : lb <= fminf(ub, wu) + E);
     const unsigned m = __ballot_sync(0xffffffffu, app);
     unsigned long long wbase = 0;
     if (lane == 0 && m) wbase = atomicAdd(&S->n_band, (unsigned long long)__popc(m));
@@ -295,7 +302,7 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
       const unsigned long long slot = wbase + __popc(m & ((1u << lane) - 1));
       if (slot < q.band_cap) {
         q.band_ids[slot] = ids;
-        q.band_d[slot] = d;
+        q.band_d[slot] = lb;
       } else {
         S->band_overflow = 1;  // the rescan pass covers every leaf pair
       }

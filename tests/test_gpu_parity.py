@@ -43,6 +43,50 @@ def test_tri_tri_fast_within_slack(md, gpu, golden, kind):
     assert err.max() <= 1.0, f"max error {err.max():.3g} x (E/2) at {int(err.argmax())}"
 
 
+def _adversarial_pairs(rng, n):
+    """Near-parallel, near-touching, sliver and coplanar triangle pairs --
+    where the float32 closest points are ill-conditioned
+    (scripts/exp_narrow_error.py has the full families)."""
+    a = rng.normal(size=(n, 3, 3))
+    out = []
+    b = a + rng.normal(size=(n, 1, 3)) * 1e-3 + rng.normal(size=(n, 3, 3)) * 10.0 ** rng.uniform(-9, -2, (n, 1, 1))
+    out.append((a, b))  # near-parallel (nearly translated copies)
+    mid = 0.5 * (a[:, 0] + a[:, 1])
+    b = rng.normal(size=(n, 3, 3))
+    b += (mid - b[:, 0])[:, None, :] + rng.normal(size=(n, 1, 3)) * 10.0 ** rng.uniform(-8, -2, (n, 1, 1))
+    out.append((a, b))  # near-touching
+    s = a.copy()
+    t = rng.uniform(size=(n, 1))
+    s[:, 2] = s[:, 0] * t + s[:, 1] * (1 - t) + rng.normal(size=(n, 3)) * 10.0 ** rng.uniform(-8, -3, (n, 1))
+    out.append((s, rng.normal(size=(n, 3, 3)) * 0.5 + rng.normal(size=(n, 1, 3))))  # slivers
+    c = rng.normal(size=(n, 3, 3))
+    c[:, :, 2] = 0.0
+    d = rng.normal(size=(n, 3, 3))
+    d[:, :, 2] = 10.0 ** rng.uniform(-9, -1, size=(n, 1))
+    out.append((c, d))  # coplanar / nearly
+    return out
+
+
+def test_tri_tri_min_lower_bound(md, gpu):
+    """The exact band windows on a conditioning-aware float32 lower bound
+    of the min distance (geometry.cuh tri_tri_min_fast_lb): it never exceeds
+    the reference's float64 distance by more than rounding (4 ulps of the
+    coordinate scale), although the raw float32 estimate overshoots it by up
+    to ~290 ulps on such pairs (beyond the band's E / 2 = 128)."""
+    from paper_2411_11244_b200.bounds import tri_tri_fast
+
+    rng = np.random.default_rng(11)
+    for fam, (a, b) in enumerate(_adversarial_pairs(rng, 1 << 17)):
+        a32, b32 = a.astype(np.float32), b.astype(np.float32)
+        lb = tri_tri_fast("min-lb", a32, b32).astype(np.float64)
+        fast = tri_tri_fast("min", a32, b32).astype(np.float64)
+        ref = md.batch_tri_tri_min(a, b)[0]
+        M = np.maximum(np.abs(a).reshape(len(a), -1).max(1), np.abs(b).reshape(len(b), -1).max(1))
+        ulp = M * 2.0 ** -23
+        assert ((lb - ref) / ulp).max() <= 4.0, fam
+        assert np.all(lb <= fast)
+
+
 @pytest.mark.parametrize("prec", [64, 32])
 def test_box_bounds_bitwise(md, gpu, golden, prec):
     dt = np.float64 if prec == 64 else np.float32
