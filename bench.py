@@ -228,8 +228,8 @@ def traverse_roofline(res, phases, bvh_a, bvh_b, kind):
     traffic = None
     tf = REPO / "profiles" / "kernel_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text())["per_launch_dram_bytes"].get(
-            "k_traverse" if kind == "min" else "k_traverse_max")
+        per = json.loads(tf.read_text())["per_launch_dram_bytes"]
+        traffic = per.get(f"k_traverse_{kind}", per.get("k_traverse" if kind == "min" else "k_traverse_max"))
     return {"bound": "hbm", "kernel": f"k_traverse_{kind} (all expansion iterations of one query, one launch)",
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
             "traffic": traffic, "peak_source": src, "algorithmic_bytes": qb["expand_bytes"], "kernel_ms": expand_ms,

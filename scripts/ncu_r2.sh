@@ -14,6 +14,10 @@ for KIND in min max; do
     > gpurun_out/prof_${TAG}_${KIND}.log 2>&1
   echo "ncu exit $?" >> gpurun_out/prof_${TAG}_${KIND}.log
 done
+# the refit kernel of one frame (both trees), ncu --set full
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_refit --launch-skip 4 --launch-count 2 \
+  -o gpurun_out/prof_${TAG}_refit -f python scripts/exp_refit.py > gpurun_out/prof_${TAG}_refit.log 2>&1
+echo "ncu exit $?" >> gpurun_out/prof_${TAG}_refit.log
 if [[ -z "$NO_SANITIZER" ]]; then
   for TOOL in memcheck racecheck synccheck; do
     timeout 900 compute-sanitizer --tool ${TOOL} --print-limit 20 --error-exitcode 9 \

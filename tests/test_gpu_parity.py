@@ -84,7 +84,7 @@ def test_tri_tri_min_lower_bound(md, gpu):
         M = np.maximum(np.abs(a).reshape(len(a), -1).max(1), np.abs(b).reshape(len(b), -1).max(1))
         ulp = M * 2.0 ** -23
         assert ((lb - ref) / ulp).max() <= 4.0, fam
-        assert np.all(lb <= fast)
+        assert np.all(lb <= fast + 4.0 * ulp)  # the estimate of another code path: rounding apart
 
 
 @pytest.mark.parametrize("prec", [64, 32])
