@@ -213,7 +213,7 @@ __device__ __forceinline__ Box leaf_box(const XfF32& x, const float4 a, const fl
   return b;
 }
 
-__global__ __launch_bounds__(128) void k_refit256(GdBvh T, XfF32 x) {
+__global__ __launch_bounds__(128, 10) void k_refit256(GdBvh T, XfF32 x) {
   constexpr int NB = kFold;  // leaves per block
   __shared__ Box wroot[4];
   __shared__ __align__(16) Box stage[kFold + kFold / 2];  // the cascade's ping-pong levels
