@@ -87,6 +87,56 @@ def test_tri_tri_min_lower_bound(md, gpu):
         assert np.all(lb <= fast + 4.0 * ulp)  # the estimate of another code path: rounding apart
 
 
+def test_near_contact_overestimate_scene(md, gpu):
+    """A scene built so that the round-1 band (windowing on the raw float32
+    distance with slack E) returned the wrong pair: triangle pair (a, b) is
+    the optimum, but its float32 distance overshoots the reference's by far
+    more than E (a near-touching, ill-conditioned configuration, ~1700 float32
+    ulps), while (a, b2) -- b2 a copy of a moved along a's normal, a few ulps
+    farther -- is estimated exactly.  With the conditioning-aware lower bound
+    the engine returns the brute-force answer."""
+    from paper_2411_11244_b200.bounds import tri_tri_fast
+
+    rng = np.random.default_rng(1)
+    n = 1 << 20
+    a = rng.normal(size=(n, 3, 3))
+    b = rng.normal(size=(n, 3, 3))
+    mid = 0.5 * (a[:, 0] + a[:, 1])
+    b += (mid - b[:, 0])[:, None, :] + rng.normal(size=(n, 1, 3)) * 10.0 ** rng.uniform(-8, -2, (n, 1, 1))
+    i = 515104
+    ta = a[i].astype(np.float32).astype(np.float64)
+    tb = b[i].astype(np.float32).astype(np.float64)
+    d1 = float(md.batch_tri_tri_min(ta[None], tb[None])[0][0])
+    nrm = np.cross(ta[1] - ta[0], ta[2] - ta[0])
+    nrm /= np.linalg.norm(nrm)
+    M = max(np.abs(ta).max(), np.abs(tb).max())
+    ulp = M * 2.0 ** -23
+    chosen = None
+    for k in range(1, 400):
+        for sgn in (1.0, -1.0):
+            tb2 = (ta + sgn * (d1 + k * ulp) * nrm).astype(np.float32).astype(np.float64)
+            d2 = float(md.batch_tri_tri_min(ta[None], tb2[None])[0][0])
+            if d1 < d2 < d1 + 30 * ulp:
+                chosen = tb2
+                break
+        if chosen is not None:
+            break
+    assert chosen is not None
+    f_opt = float(tri_tri_fast("min", ta[None].astype(np.float32), tb[None].astype(np.float32))[0])
+    f_alt = float(tri_tri_fast("min", ta[None].astype(np.float32), chosen[None].astype(np.float32))[0])
+    E = 2.0 ** -15 * max(M, np.abs(chosen).max())
+    assert f_opt > f_alt + E  # the raw float32 window would have dropped the optimum
+    A = md.TriangleMesh(ta, np.array([[0, 1, 2]]))
+    B = md.TriangleMesh(np.concatenate([tb, chosen]), np.array([[0, 1, 2], [3, 4, 5]]))
+    for prec, dt in ((64, np.float64), (32, np.float32)):
+        tA, tB = md.build_f12(A, dtype=dt), md.build_f12(B, dtype=dt)
+        r = md.run_min_query(A, B, tA, tB, md.EngineConfig(precision=prec))
+        d, w = md.brute_force_min(A, B, dtype=dt)
+        assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (w.tri_a, w.tri_b), prec
+        if prec == 64:
+            assert (w.tri_a, w.tri_b) == (0, 0)  # the ill-conditioned pair is the float64 optimum
+
+
 @pytest.mark.parametrize("prec", [64, 32])
 def test_box_bounds_bitwise(md, gpu, golden, prec):
     dt = np.float64 if prec == 64 else np.float32
