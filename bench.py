@@ -172,11 +172,16 @@ class ClockSampler:
             self._stop.wait(0.0005 if self._nv is not None else 0.1)
 
     def __enter__(self):
+        # the launching thread holds the GIL between its ctypes calls: a short
+        # switch interval lets the sampler run every ~0.5 ms during the region
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(1e-4)
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        sys.setswitchinterval(self._switch)
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
@@ -377,6 +382,7 @@ def frame_graph_section(md, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red
         fg.close()
     # host wall clock through the public API (transforms in, records out)
     tz, tb, xfs = seq  # the base meshes and the timed frames' transforms
+    md.run_sequence_minmax(tz, tb, bvh_a, bvh_b, xfs[:2], ("min", "max"), cfg)  # its two graphs, captured once
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     out = md.run_sequence_minmax(tz, tb, bvh_a, bvh_b, xfs, ("min", "max"), cfg)
