@@ -49,7 +49,12 @@ typedef struct GdMesh {
   double rot[9];
   double trans[3];
   int32_t has_xf;
-  int32_t _pad;
+  /* operation order of the float64 transform, matching the host BLAS that
+   * the reference's `V @ R.T + t` (mesh.py:104) runs on, so moved vertices
+   * are bitwise the reference's: 0 = fma(R2, z, fma(R1, y, R0 x)) (OpenBLAS
+   * dgemm, this image), 1 = (R0 x + R1 y) + R2 z without FMA, 2 =
+   * fma(R0, x, fma(R1, y, R2 z)); then + t.  Probed once per process. */
+  int32_t xf_order;
 } GdMesh;
 
 /* Sizes of an f12-BVH over m triangles (bvh.py:98-111, 184-211). */

@@ -37,7 +37,7 @@ class GdMesh(C.Structure):
         ("rot", C.c_double * 9),
         ("trans", C.c_double * 3),
         ("has_xf", C.c_int32),
-        ("_pad", C.c_int32),
+        ("xf_order", C.c_int32),
     ]
 
 

@@ -255,14 +255,20 @@ __device__ __forceinline__ Box tri_box(const Tri<float>& t) {
 // over k with fused multiply-adds, x' = fma(R02, z, fma(R01, y, R00 x)), and
 // the translation is a separate add -- reproduced here, so a moved mesh has
 // the reference's vertex bits (tests/test_gpu_parity.py).
+// one row of R v in the host BLAS's order (GdMesh.xf_order)
+__device__ __forceinline__ double xf_row(const double* r, double x, double y, double z, int order) {
+  if (order == 1) return __dadd_rn(__dadd_rn(__dmul_rn(r[0], x), __dmul_rn(r[1], y)), __dmul_rn(r[2], z));
+  if (order == 2) return __fma_rn(r[0], x, __fma_rn(r[1], y, __dmul_rn(r[2], z)));
+  return __fma_rn(r[2], z, __fma_rn(r[1], y, __dmul_rn(r[0], x)));
+}
 __device__ __forceinline__ V3<double> mesh_vertex(const GdMesh& m, long long i) {
   const double* p = m.vtx + 3 * i;
   double x = p[0], y = p[1], z = p[2];
   if (!m.has_xf) return {x, y, z};
   const double* R = m.rot;
-  return {__dadd_rn(__fma_rn(R[2], z, __fma_rn(R[1], y, __dmul_rn(R[0], x))), m.trans[0]),
-          __dadd_rn(__fma_rn(R[5], z, __fma_rn(R[4], y, __dmul_rn(R[3], x))), m.trans[1]),
-          __dadd_rn(__fma_rn(R[8], z, __fma_rn(R[7], y, __dmul_rn(R[6], x))), m.trans[2])};
+  return {__dadd_rn(xf_row(R, x, y, z, m.xf_order), m.trans[0]),
+          __dadd_rn(xf_row(R + 3, x, y, z, m.xf_order), m.trans[1]),
+          __dadd_rn(xf_row(R + 6, x, y, z, m.xf_order), m.trans[2])};
 }
 
 template <typename T>

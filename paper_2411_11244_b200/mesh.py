@@ -203,6 +203,7 @@ class TriangleMesh:
             g.rot[:] = [float(x) for x in self._rot.reshape(9)]
             g.trans[:] = [float(x) for x in self._trans.reshape(3)]
             g.has_xf = 1
+            g.xf_order = blas_order()
         self._gview = g
         return g
 
@@ -263,6 +264,44 @@ class RigidTransform:
 
     def __repr__(self) -> str:
         return f"RigidTransform(rotation={self.rotation.tolist()}, translation={self.translation.tolist()})"
+
+
+_BLAS_ORDER = None
+
+
+def _fma(a: float, b: float, c: float) -> float:
+    """Correctly rounded a * b + c (exact rational arithmetic; for probes)."""
+    from fractions import Fraction
+
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+def blas_order() -> int:
+    """Operation order of numpy's `V @ R.T` on this host (GdMesh.xf_order):
+    probed once on random rows against the candidate orders, so the device
+    transform reproduces the reference's float64 vertices bit for bit
+    whatever BLAS numpy links.  0 (OpenBLAS dgemm on this image) when no
+    candidate matches -- then moved vertices agree to an ulp, not bitwise."""
+    global _BLAS_ORDER
+    if _BLAS_ORDER is not None:
+        return _BLAS_ORDER
+    rng = np.random.default_rng(12345)
+    V = rng.normal(size=(257, 3)) * 10.0 ** rng.uniform(-3, 3, size=(257, 1))
+    R = rng.normal(size=(3, 3))
+    got = V @ R.T
+    cands = {
+        0: lambda r, v: _fma(r[2], v[2], _fma(r[1], v[1], r[0] * v[0])),
+        1: lambda r, v: (r[0] * v[0] + r[1] * v[1]) + r[2] * v[2],
+        2: lambda r, v: _fma(r[0], v[0], _fma(r[1], v[1], r[2] * v[2])),
+    }
+    order = 0
+    for k, f in cands.items():
+        if all(got[i, j] == f([float(x) for x in R[j]], [float(x) for x in V[i]])
+               for i in range(len(V)) for j in range(3)):
+            order = k
+            break
+    _BLAS_ORDER = order
+    return order
 
 
 def apply_transform(mesh: TriangleMesh, xf: RigidTransform) -> TriangleMesh:

@@ -264,3 +264,27 @@ def test_integration_doc_lists_every_entry_point():
     names = set(re.findall(r"^\w[\w\s\*]*?\b(gd_\w+)\(", (root / "include" / "gdist.h").read_text(), re.M))
     doc = (root / "INTEGRATION.md").read_text()
     assert names and not [n for n in sorted(names) if n not in doc]
+
+
+def test_blas_order_probe_reproduces_numpy():
+    """GdMesh.xf_order: the probed operation order reproduces numpy's
+    `V @ R.T` (the reference's apply_transform, mesh.py:104) bit for bit on
+    fresh data, so the device transform gives the reference's vertices."""
+    import numpy as np
+
+    from paper_2411_11244_b200 import mesh
+
+    order = mesh.blas_order()
+    assert order in (0, 1, 2)
+    rng = np.random.default_rng(7)
+    V = rng.normal(size=(200, 3)) * 10.0 ** rng.uniform(-4, 4, size=(200, 1))
+    R = rng.normal(size=(3, 3))
+    got = V @ R.T
+    f = mesh._fma
+    for i in range(len(V)):
+        for j in range(3):
+            r, v = [float(x) for x in R[j]], [float(x) for x in V[i]]
+            want = {0: f(r[2], v[2], f(r[1], v[1], r[0] * v[0])),
+                    1: (r[0] * v[0] + r[1] * v[1]) + r[2] * v[2],
+                    2: f(r[0], v[0], f(r[1], v[1], r[2] * v[2]))}[order]
+            assert got[i, j] == want, (i, j, order)
