@@ -284,6 +284,15 @@ def measure_query(md, _lib, a, b, ta, tb, kind, cfg, reps=5):
         rl = traverse_roofline(res, phases, ta, tb, kind)
         rl["traffic"] = None  # the committed ncu DRAM capture is of the rings workload only
         out["roofline"] = rl
+        # the narrow phase against the FP32 CUDA-core peak (per
+        # tested triangle pair ~2100 flop for min, 72 for max; nominal peak)
+        flop = res.narrow_pairs * (2100 if kind == "min" else 72)
+        if phases["narrow"] > 0:
+            tf = flop / (phases["narrow"] * 1e-3) / 1e12
+            out["narrow_fp32"] = {"bound": "fp32", "achieved": round(tf, 3), "peak": FP32_PEAK_TFLOPS,
+                                  "unit": "TFLOP/s", "frac": round(tf / FP32_PEAK_TFLOPS, 4),
+                                  "peak_source": "nominal (148 SM x 128 lanes x 2 x 1.965 GHz)",
+                                  "flop": int(flop), "narrow_ms": round(phases["narrow"], 6)}
     else:
         out["roofline"] = None
         out["roofline_note"] = "chunked traversal (the front outgrew the arena): per-round phases not timed"
@@ -510,6 +519,9 @@ def split_section(md, tz, tb, bvh_a, bvh_b, cfg, kind, dist, red_dev, backend, f
                    "latency bound (fronts < 25K entries), so the split pays only on large queries")
     out["backend"] = backend
     return {"split": out}
+
+
+FP32_PEAK_TFLOPS = 74.4
 
 
 def peaks():
