@@ -78,7 +78,11 @@ def _worker(rank, world, port, q):
         za, zb = md.build_f12(tz), md.build_f12(tbase)
         xfs = [md.ring_frame_transforms(f) for f in range(0, 70, 10)]
         seq = md.run_sequence(tz, tbase, za, zb, xfs, "min")
+        # config 3 on the ranks: frames sharded, each frame one CUDA graph replay
+        both = md.run_sequence_minmax(tz, tbase, za, zb, xfs)
+        out["graph_min_equal"] = bool(np.array_equal(both["min"], seq))
         md.parallel.release_split_plans()
+        md.parallel.release_frame_graphs()
         q.put((rank, out, seq.tolist()))
     finally:
         dist.destroy_process_group()
@@ -126,6 +130,7 @@ def test_two_processes_gloo(md, gpu):
             # with its own bound alone (same cells, tighter or equal bound)
             ipc, local, ar = out[kind + "_work"]
             assert ipc <= local * 1.02 and ar <= local * 1.02, (rank, kind, out[kind + "_work"])
+        assert out["graph_min_equal"], rank
         assert np.array_equal(np.asarray(seq), np.asarray(want_seq, dtype=np.float64)), rank
 
 

@@ -323,6 +323,17 @@ def test_rotation_frames_golden_sequence_paths(md, gpu, golden_meta):
     fg.close()
     with pytest.raises(ValueError):
         md.FrameGraph(a0, b0, bvh_a, bvh_b, ("median",))
+    # a chunked traversal (an arena far too small for the fronts): the graph's
+    # record says `pending` and the remaining rounds run after the replay
+    cfg = md.EngineConfig(arena_entries=1 << 11, front_hard_cap=1 << 30)
+    fg = md.FrameGraph(a0, b0, bvh_a, bvh_b, ("min", "max"), cfg)
+    for rec, (xa, xb) in list(zip(recs, xfs))[:3]:
+        a, b = md.apply_transform(tz, xa), md.apply_transform(tb, xb)
+        out = fg.run(a, b)
+        for q in ("min", "max"):
+            assert (out[q].distance, out[q].witness.tri_a, out[q].witness.tri_b) == (
+                rec[q]["distance"], rec[q]["tri_a"], rec[q]["tri_b"]), (rec["frame"], q, "chunked")
+    fg.close()
 
 
 def test_brute_force_device(md, gpu, golden_meta):
