@@ -75,6 +75,10 @@ static void validate(const GdBvh& a, const GdBvh& b, const GdConfig& cfg) {
            "tree depth out of range");
   GD_CHECK(a.box && b.box && a.leaf_rec && b.leaf_rec && a.vtx32 && b.vtx32 && a.vmap && b.vmap,
            GD_ERR_INVALID, "BVH arrays must be allocated");
+  // the box and leaf_tri gathers use 256-bit loads (engine.cuh)
+  GD_CHECK(((reinterpret_cast<uintptr_t>(a.box) | reinterpret_cast<uintptr_t>(b.box) |
+             reinterpret_cast<uintptr_t>(a.leaf_tri) | reinterpret_cast<uintptr_t>(b.leaf_tri)) & 31) == 0,
+           GD_ERR_INVALID, "BVH box / leaf_tri buffers must be 32-byte aligned");
 }
 
 // optional phase timing for the bench: events between the query phases

@@ -9,6 +9,18 @@
 
 namespace gd {
 
+// Device schedule (GdConfig.schedule >= 0): k = 1 sweeps of fronts of at
+// least this many entries take the bound update (the enhanced bound of each
+// entry's most promising kept child pair, ~90 instructions) from the first
+// round of every tile only -- a quarter of the entries.  By then the bound
+// has converged (rings: it moves by < 1e-4 relative over the last five
+// iterations), any kept pair's bound is valid, and the sweeps are issue /
+// latency bound: rings min expand 0.252 -> 0.244 ms.  The reference schedule
+// (-1) updates from every entry, as query.py:416-423.
+#ifndef GD_K1_THIN_BOUND
+#define GD_K1_THIN_BOUND 200000u
+#endif
+
 // ownership test compiled out of the single-GPU traversal (kSplit = false):
 // the sweeps run at 64 registers, and every live value counts
 template <bool kSplit>
@@ -306,6 +318,7 @@ __device__ __forceinline__ void k1_sweep(const QArgs& q, ExpandShared& sh, unsig
   float* s_key = reinterpret_cast<float*>(stage + kK1Stage * sizeof(uint2));
   const int ca = 1 << ka, cb = 1 << kb;
   const int lane = threadIdx.x & 31;
+  const bool thin_bound = q.cfg.schedule >= 0 && n_in >= (unsigned)GD_K1_THIN_BOUND;
   // even contiguous split of the chunk over the blocks (no tail imbalance at
   // the grid barrier), processed in tiles of <= kK1Rounds rounds of one entry
   // per thread
@@ -377,7 +390,7 @@ __device__ __forceinline__ void k1_sweep(const QArgs& q, ExpandShared& sh, unsig
           // most promising kept child pair: any kept pair's enhanced bound
           // is a valid bound (query.py:416-423 takes the minimum over all
           // kept pairs -- same fixed point, a quarter of the arithmetic)
-          if (keep && !to_leaves) {
+          if (keep && !to_leaves && (r == 0 || !thin_bound)) {
             const Box ba = select_box((bc >> 1) != 0, A[1], A[0]);
             const Box bb = select_box((bc & 1) != 0, B[1], B[0]);
             const float u = pair_update<kMax>(ba, bb, enh);
