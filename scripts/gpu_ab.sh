@@ -21,6 +21,6 @@ for f in sorted(glob.glob('gpurun_out/ab_*.log')):
         d = json.loads(line)
         if d['warm']: continue
         print(f, d['distance'], d['witness'], d['phases_ms'])
-        print('   ', [(i['in'], i['ms']) for i in d['iters']])
+        print('   ', [(i['in'], i['k'], i['ms']) for i in d['iters']])
 PY
 for s in ${EXTRA:-}; do timeout 300 python $s > gpurun_out/$(basename $s .py).log 2>&1; cat gpurun_out/$(basename $s .py).log | tail -5; done
