@@ -86,11 +86,10 @@ struct alignas(16) QState {
   unsigned dfs_coord;                // per-triangle DFS: max |coordinate| of A (float bits)
   unsigned long long visited;        // per-triangle DFS: node examinations
   unsigned long long cnt[3];                   // sweep i % 3: survivors (low 40 bits) + arrivals
-  unsigned long long culled_it[kMaxIters];     // reference-equivalent candidates culled, per iteration
   unsigned long long skip_it[kMaxIters];       // candidates of pairs another split rank owns
   unsigned long long tot_cand[kMaxIters];      // candidates expanded per iteration (all chunks)
   unsigned long long tot_in[kMaxIters];        // front entries expanded per iteration
-  unsigned long long tot_out[kMaxIters];       // survivors per iteration
+  unsigned long long tot_out[kMaxIters];       // survivors per iteration (leaf pairs for the last)
   Level lv[kMaxLevels];              // the front stack (persists across rounds)
   GdResult res;                      // the result record, then the stats: one
   GdIterStat stats[kMaxIters];       // contiguous device->host copy

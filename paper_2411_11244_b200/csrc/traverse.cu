@@ -179,7 +179,6 @@ struct ExpandShared {
   unsigned long long out_base;
   unsigned warp_tot[kExpandThreads / 32];
   float warp_upd[2][kExpandThreads / 32];
-  unsigned long long red_culled[kExpandThreads / 32];
   unsigned stage_count;
 };
 
@@ -275,21 +274,16 @@ __device__ __forceinline__ unsigned warp_append(unsigned* counter, unsigned cnt)
   return wbase + incl - cnt;
 }
 
-// per-block totals of the reference-equivalent culled / skipped candidates
-__device__ __forceinline__ void sweep_counters(QState* S, ExpandShared& sh, int it, unsigned long long my_culled,
+// Every candidate of a sweep is culled, survives, or (split query) belongs
+// to another rank, so an iteration's reference-equivalent culled count is
+// derived from its totals (write_stat): only the skipped candidates of a
+// split query are counted, per warp.  (my_culled stays in the sweeps as the
+// reference's accounting; the compiler drops it.)
+__device__ __forceinline__ void sweep_counters(QState* S, ExpandShared&, int it, unsigned long long,
                                                unsigned long long my_skipped, bool split) {
-  const unsigned long long c = warp_sum_u64(my_culled);
-  const unsigned long long sk = split ? warp_sum_u64(my_skipped) : 0ull;
-  if ((threadIdx.x & 31) == 0) {
-    sh.red_culled[threadIdx.x >> 5] = c;
-    if (sk) atomicAdd(&S->skip_it[it], sk);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long bc = 0;
-    for (int w = 0; w < kExpandThreads / 32; ++w) bc += sh.red_culled[w];
-    if (bc) atomicAdd(&S->culled_it[it], bc);
-  }
+  if (!split) return;
+  const unsigned long long sk = warp_sum_u64(my_skipped);
+  if ((threadIdx.x & 31) == 0 && sk) atomicAdd(&S->skip_it[it], sk);
 }
 
 // k == 1 sweep (the wide late iterations): one thread per front entry; it
@@ -775,7 +769,7 @@ __device__ __noinline__ void commit_sweep(const QArgs& q, TravShared& t, const S
   const unsigned long long ncand = p.c << (p.ka + p.kb);
   t.tot_cand[it] += ncand;
   t.tot_in[it] += p.c;
-  if (!p.to_leaves) t.tot_out[it] += n_out;
+  t.tot_out[it] += n_out;  // survivors: front entries, or leaf pairs for the narrow phase
   t.iter = max(t.iter, it + 1);
   if (rec) {
     // the statistics are written during the next sweep (stat_pending): their
@@ -841,7 +835,8 @@ __device__ __forceinline__ void write_stat(QState* S, TravShared& t) {
   st.k = t.stat_k;
   st.front_in = (long long)t.tot_in[it];
   st.front_out = t.stat_leaf ? 0 : (long long)t.tot_out[it];
-  st.culled = (long long)V->culled_it[it];
+  // culled = candidates - survivors - (split query) candidates other ranks own
+  st.culled = (long long)(t.tot_cand[it] - t.tot_out[it] - V->skip_it[it]);
   const float b = __uint_as_float(V->bound_bits);
   st.bound_after = kMax ? (double)b + (double)S->slack : (double)b - (double)S->slack;
   st._pad = 0;
@@ -877,7 +872,6 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
       // per-iteration counters, zeroed by block 0's threads in parallel (the
       // grid barrier below publishes them)
       for (int i = threadIdx.x; i < kMaxIters; i += blockDim.x) {
-        S->culled_it[i] = 0;
         S->skip_it[i] = 0;
         S->t_sweep[i] = 0;
         S->tot_cand[i] = 0;
