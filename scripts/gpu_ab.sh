@@ -8,6 +8,8 @@ if [[ -z $NOTESTS ]]; then
   tail -3 gpurun_out/pytest_gpu.log
 fi
 for v in ${VARIANTS:-libgdist.so}; do
+  echo "$v production per-frame:"; GDIST_LIB_VARIANT=$v timeout 300 python scripts/exp_frames_query.py | tail -1
+  [[ -n $NOANATOMY ]] && continue
   for kind in min max; do
     GDIST_LIB_VARIANT=$v timeout 300 python scripts/exp_query.py 2500 1500 7 $kind > gpurun_out/ab_${v%.so}_$kind.log 2>&1
   done
