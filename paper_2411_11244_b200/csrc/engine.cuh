@@ -81,11 +81,11 @@ struct alignas(16) QState {
   long long ov_cand, ov_in, ov_cap;
   float slack;
   int band_overflow;
-  unsigned bar;                      // grid-barrier arrivals (k_traverse)
   unsigned fbest;                    // best float32 narrow distance (ordered bits)
   unsigned dfs_coord;                // per-triangle DFS: max |coordinate| of A (float bits)
   unsigned long long visited;        // per-triangle DFS: node examinations
   unsigned long long cnt[3];                   // sweep i % 3: survivors (low 40 bits) + arrivals
+  unsigned long long epoch_flag;                // k_traverse: the launch epoch whose prologue is done
   unsigned long long skip_it[kMaxIters];       // candidates of pairs another split rank owns
   unsigned long long tot_cand[kMaxIters];      // candidates expanded per iteration (all chunks)
   unsigned long long tot_in[kMaxIters];        // front entries expanded per iteration
@@ -107,6 +107,7 @@ struct QArgs {
   int mode;       // 0: a round resumes after a leaf chunk; 1: continue a query paused at its sweep budget
                   //    (a no-op once its traversal ended) -- the split query's bound-exchange rounds
   int sweep_budget;  // expansion sweeps this launch may run (0 = no limit)
+  unsigned long long epoch;     // unique per k_traverse launch (query.cu next_epoch)
   GdBvh A, B;
   GdConfig cfg;
   QState* S;

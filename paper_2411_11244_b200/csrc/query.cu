@@ -1,7 +1,6 @@
 // query.cu -- host orchestration of a BVTT distance query (query.py:480-568).
 //
 // One query = a fixed launch sequence on one stream, no host round trip:
-//   memset            grid-barrier counter
 //   k_traverse        ONE persistent cooperative launch: root bounds, slack,
 //                     root front (query.py:454-509), then every adaptive-depth
 //                     expansion (query.py:349-451) separated by grid barriers
@@ -20,6 +19,8 @@
 // (DESIGN.md "Exactness"): culling is conservative, so every pair that can
 // attain the reference's exact answer reaches the exact pass.
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstddef>
 #include <cstring>
 
@@ -155,13 +156,22 @@ static unsigned refine_grid() {
   return g[dev];
 }
 
-// memset of the grid-barrier counter + the persistent traversal kernel
+// k_traverse launch epochs: unique per launch within the process (odd,
+// strictly increasing by 2), seeded away from values a fresh workspace might
+// hold (0, small counters)
+unsigned long long next_epoch() {
+  static std::atomic<unsigned long long> e{
+      (0x9E3779B97F4A7C15ull ^ (unsigned long long)std::chrono::steady_clock::now().time_since_epoch().count()) |
+      (1ull << 62) | 1ull};
+  return e.fetch_add(2, std::memory_order_relaxed);
+}
+
+// the persistent traversal kernel (its prologue initialises the state; no
+// memset before it: the blocks meet on the launch's epoch, traverse.cu)
 template <bool kMax>
-static void launch_traverse(const QArgs& q, cudaStream_t s) {
+static void launch_traverse(QArgs q, cudaStream_t s) {
   const int sms = num_sms();
-  // the grid-barrier counter must start at 0; everything else is initialised
-  // by k_traverse's prologue
-  GD_CUDA(cudaMemsetAsync(&q.S->bar, 0, sizeof(unsigned), s));
+  q.epoch = next_epoch();
   if (g_profile) GD_CUDA(cudaEventRecord(g_ev[1], s));
   // persistent traversal: as many blocks as can be co-resident (cooperative
   // launch guarantees it; the grid barrier relies on it); the split-query
@@ -192,7 +202,7 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
     if (g_profile) GD_CUDA(cudaEventRecord(g_ev[i], s));
   };
   mark(0);
-  launch_traverse<kMax>(q, s);  // records g_ev[1] between the memset and the kernel
+  launch_traverse<kMax>(q, s);  // records g_ev[1] before the kernel
   // the node boxes are read by k_traverse only: a refit for the next frame
   // may start once this event has fired
   if (traversal_done) GD_CUDA(cudaEventRecord(traversal_done, s));
@@ -269,6 +279,7 @@ bool is_query_kernel(const void* f) {
 }
 
 void retransform(QArgs& q, const GdMesh& ma, const GdMesh& mb) {
+  q.epoch = next_epoch();  // a replayed k_traverse node needs a fresh launch epoch
   GD_CHECK(ma.vtx == q.ma.vtx && mb.vtx == q.mb.vtx && ma.m == q.ma.m && mb.m == q.mb.m, GD_ERR_TOPOLOGY,
            "a frame graph replays the meshes it was captured with (same base vertices), moved");
   q.ma = ma;

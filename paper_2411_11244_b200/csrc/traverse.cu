@@ -208,6 +208,13 @@ __device__ __forceinline__ unsigned long long out_slot(const SweepPlan& p, unsig
 template <bool kMax>
 __device__ __forceinline__ void write_stat(QState* S, TravShared& t);
 
+// A grid barrier that can never complete (a bug) must not hang the GPU:
+// after ~2^26 polls (tens of seconds; a sweep's barrier takes microseconds)
+// the kernel traps -- the launch fails loudly with an error instead.
+__device__ __forceinline__ void spin_watchdog(unsigned polls) {
+  if (polls == (1u << 26)) __trap();
+}
+
 // Grid-wide barrier of the persistent traversal (all blocks co-resident:
 // cooperative launch).  `bar` only grows; phase p completes when it reaches
 // p * gridDim.x, so no reset is needed inside a launch.
@@ -236,8 +243,10 @@ __device__ __forceinline__ unsigned long long count_barrier(unsigned long long* 
     asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(cnt), "l"(1ull << kArriveShift) : "memory");
     if (stat) write_stat<kMax>(S, *stat);
     unsigned long long v;
+    unsigned polls = 0;
     do {
       asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(cnt) : "memory");
+      spin_watchdog(++polls);
     } while ((v & ~((1ull << kArriveShift) - 1)) < target);
     total = v & ((1ull << kArriveShift) - 1);
   }
@@ -245,15 +254,25 @@ __device__ __forceinline__ unsigned long long count_barrier(unsigned long long* 
   return total;
 }
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned phase) {
+// The launch's start: block 0 runs the prologue, then publishes the launch's
+// epoch (unique per launch, from the host); every other block waits for it.
+// Nothing else crosses blocks before the first sweep barrier, so no counted
+// grid barrier -- and no counter to reset with a memset before the launch --
+// is needed.  A workspace's stale flag is an older epoch of this process (or
+// garbage), never the current one.
+__device__ __forceinline__ void prologue_barrier(unsigned long long* flag, unsigned long long epoch) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned target = phase * gridDim.x;
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
+    if (blockIdx.x == 0) {
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flag), "l"(epoch) : "memory");
+    } else {
+      unsigned long long v;
+      unsigned polls = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+        spin_watchdog(++polls);
+      } while (v != epoch);
+    }
   }
   __syncthreads();
 }
@@ -868,7 +887,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
   const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
   if (blockIdx.x == 0) {
     if (q.round == 0) {
-      if (threadIdx.x == 0) init_query<kMax>(q);  // S->bar was zeroed by the host (memset node)
+      if (threadIdx.x == 0) init_query<kMax>(q);
       // per-iteration counters, zeroed by block 0's threads in parallel (the
       // grid barrier below publishes them)
       for (int i = threadIdx.x; i < kMaxIters; i += blockDim.x) {
@@ -883,7 +902,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
     }
     if (threadIdx.x < 3) S->cnt[threadIdx.x] = 0;
   }
-  grid_barrier(&S->bar, 1);
+  prologue_barrier(&S->epoch_flag, q.epoch);
   for (int i = threadIdx.x; i < kMaxIters; i += blockDim.x) {
     t.tot_cand[i] = V->tot_cand[i];
     t.tot_in[i] = V->tot_in[i];
