@@ -362,11 +362,14 @@ def configs_section(md, _lib):
 
 
 def frame_graph_section(md, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_dev, seq):
-    """Config 3 with each frame (refit A + refit B + min + max + the two
-    record copies) replayed as ONE CUDA graph (FrameGraph): device ms per
-    frame (CUDA events around K back-to-back replays, max over ranks) and
-    the host wall clock of run_sequence_minmax over the same K frames (records read
-    back per frame), beside the stream-launched frame above."""
+    """Config 3 through its public API, run_sequence_minmax: each frame
+    (refit A + refit B + min + max + the two record copies) is one CUDA graph
+    replay (FrameGraph); two graphs alternate on two streams so frame f + 1's
+    refits overlap frame f's narrow / exact phases.  Device ms per frame =
+    CUDA events on the calling stream around the whole K-frame call (the call
+    joins its streams into it), max over ranks; e2e = the host wall clock of
+    the same call (transforms in, every frame's records read back); plus one
+    graph replayed back to back without the overlap."""
     import torch
 
     a0, b0, _ = prepared[0]
@@ -385,27 +388,44 @@ def frame_graph_section(md, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red
             fg.launch(a, b)
         e.record(stream)
         torch.cuda.synchronize()
-        dev_ms = s.elapsed_time(e) / K
-        last = fg.results()
+        single_ms = s.elapsed_time(e) / K
     finally:
         fg.close()
-    # host wall clock through the public API (transforms in, records out)
     tz, tb, xfs = seq  # the base meshes and the timed frames' transforms
     md.run_sequence_minmax(tz, tb, bvh_a, bvh_b, xfs[:2], ("min", "max"), cfg)  # its two graphs, captured once
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
     t0 = time.perf_counter()
     out = md.run_sequence_minmax(tz, tb, bvh_a, bvh_b, xfs, ("min", "max"), cfg)
+    e.record(stream)
+    torch.cuda.synchronize()
     host_ms = (time.perf_counter() - t0) * 1e3 / K
+    dev_ms = s.elapsed_time(e) / K
+    from paper_2411_11244_b200.parallel import release_frame_graphs
+
+    release_frame_graphs()
+    # the job's last frame through the plain API: the same answers
+    a, b = md.apply_transform(tz, xfs[-1][0]), md.apply_transform(tb, xfs[-1][1])
+    md.refit(bvh_a, a)
+    md.refit(bvh_b, b)
+    ref = (md.run_min_query(a, b, bvh_a, bvh_b, cfg), md.run_max_query(a, b, bvh_a, bvh_b, cfg))
     if dist:
-        t = torch.tensor([dev_ms, host_ms], device=red_dev)
+        t = torch.tensor([dev_ms, host_ms, single_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms, host_ms = float(t[0].item()), float(t[1].item())
+        dev_ms, host_ms, single_ms = float(t[0].item()), float(t[1].item()), float(t[2].item())
     return {"frame_min_max_graph_ms": round(dev_ms, 6), "frame_min_max_graph_e2e_ms": round(host_ms, 6),
-            "frame_min_max_graph_note": "config 3 per frame as one CUDA graph replay (FrameGraph: refit A + refit B "
-                                        "+ min + max + record copies); e2e = host wall clock of run_sequence_minmax "
-                                        "(records read back per frame, two graphs alternating)",
-            "frame_graph_answers_equal": bool(last["min"].distance == out["min"][-1][0]
-                                              and last["max"].distance == out["max"][-1][0])}
+            "frame_min_max_graph_single_ms": round(single_ms, 6),
+            "frame_min_max_graph_note": "config 3 through run_sequence_minmax: per frame one CUDA graph replay "
+                                        "(refit A + refit B + min + max + record copies), two graphs alternating "
+                                        "on two streams so frame f+1's refits overlap frame f's narrow / exact "
+                                        "phases; device ms = CUDA events around the whole call / K, e2e = its host "
+                                        "wall clock (records read back per frame); _single_ms: one graph "
+                                        "replayed back to back",
+            "frame_graph_answers_equal": bool(ref[0].distance == out["min"][-1][0]
+                                              and ref[1].distance == out["max"][-1][0])}
 
 
 def max_section(md, _lib, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_dev, seq):
@@ -439,11 +459,41 @@ def max_section(md, _lib, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_d
         ev[j][3].record(stream)
     torch.cuda.synchronize()
     max_ms = float(np.mean([e[2].elapsed_time(e[3]) for e in ev]))
-    frame_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in ev]))
+    seq_frame_ms = float(np.mean([e[0].elapsed_time(e[3]) for e in ev]))
+    # the same frames with the two queries as one group (md.launch_group):
+    # traversals back to back, the two narrow / exact chains side by side
+    # (a group's queries need distinct workspaces: two private plans, bound
+    # to each frame's moved meshes)
+    a0, b0, _ = prepared[0]
+    gmin = md.PreparedQuery(a0, b0, bvh_a, bvh_b, cfg, "min", private_workspace=True)
+    gmax = md.PreparedQuery(a0, b0, bvh_a, bvh_b, cfg, "max", private_workspace=True)
+    gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(K)]
+    for j, i in enumerate(list(range(W)) + list(range(W, W + K))):
+        a, b, pq = prepared[i]
+        if j >= W:
+            gev[j - W][0].record(stream)
+        bvh_a._device_refit(a)
+        bvh_b._device_refit(b)
+        gmin.bind(a, b)
+        gmax.bind(a, b)
+        md.launch_group([gmin, gmax])
+        if j >= W:
+            gev[j - W][1].record(stream)
+    torch.cuda.synchronize()
+    frame_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in gev]))
+    # the last frame's grouped answers equal its separate ones
+    gres = (gmin.collect(), gmax.collect())
+    sres = []
+    for pq in (prepared[-1][2], plans[-1]):  # the boxes describe the last frame
+        pq.launch()
+        sres.append(pq.collect())
+    group_equal = all(g.distance == r.distance and (g.witness.tri_a, g.witness.tri_b) == (r.witness.tri_a, r.witness.tri_b)
+                      for g, r in zip(gres, sres))
+    del gmin, gmax
     if dist:
-        t = torch.tensor([max_ms, frame_ms], device=red_dev)
+        t = torch.tensor([max_ms, frame_ms, seq_frame_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        max_ms, frame_ms = float(t[0].item()), float(t[1].item())
+        max_ms, frame_ms, seq_frame_ms = float(t[0].item()), float(t[1].item()), float(t[2].item())
     # answers and the profiled phases of the last frame's max query
     L = _lib.lib()
     a, b, _ = prepared[-1]
@@ -461,7 +511,11 @@ def max_section(md, _lib, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_d
             "max_distance": res.distance, "max_witness": [res.witness.tri_a, res.witness.tri_b],
             "max_roofline": traverse_roofline(res, phases, bvh_a, bvh_b, "max"),
             "frame_min_max_ms": round(frame_ms, 6),
-            "frame_min_max_note": "config 3 per frame: refit A + refit B + min + max, back to back on one stream"}, res
+            "frame_min_max_sequential_ms": round(seq_frame_ms, 6),
+            "frame_min_max_group_answers_equal": bool(group_equal),
+            "frame_min_max_note": "config 3 per frame: refit A + refit B + min + max as one query group (traversals "
+                                  "back to back, the two narrow / exact chains side by side on forked streams); "
+                                  "_sequential_ms: the two queries back to back on one stream"}, res
 
 
 def split_section(md, tz, tb, bvh_a, bvh_b, cfg, kind, dist, red_dev, backend, frame=7, reps=5):
@@ -684,7 +738,8 @@ def run_ours(args):
     max_keys, max_res = {}, None
     if not args.no_max and args.kind == "min" and not args.profile_only:
         max_keys, max_res = max_section(md, _lib, bvh_a, bvh_b, prepared, W, K, cfg, stream, dist, red_dev,
-                                        (tz, tb, [md.ring_frame_transforms(f % 1000) for f in frames[W:W + K]]))
+                                        (tz, tb, [md.ring_frame_transforms(f % 1000)
+                                                  for f in range(W * N, (W + K) * N)]))
     # one query split over the N ranks, max over ranks
     split_keys = {}
     if N > 1 and not args.profile_only:

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define GDIST_ABI_VERSION 14
+#define GDIST_ABI_VERSION 15
 
 /* Status codes; the Python layer maps them onto errors.py (errors.py:8-69). */
 typedef enum GdStatus {
@@ -315,19 +315,38 @@ int gd_query_traverse(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a
 int gd_query_finish(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                     const GdConfig* cfg, void* workspace, size_t workspace_bytes, GdResult* result_dev,
                     void* stream);
+/* Several queries on the same trees and meshes (config 3: the min and max
+ * query of one frame), each on its own workspace: their traversals back to
+ * back on `stream` (each needs the whole GPU), then every query's narrow /
+ * exact chain on its own stream, forked after the last traversal and joined
+ * back into `stream` -- the short, latency-bound chains overlap.  n in
+ * [1, 8]; host_dst[i] (pinned, may be NULL) receives query i's result record
+ * + max_stats GdIterStat at the end of its chain; traversal_done (a
+ * cudaEvent_t or NULL) is recorded after the last traversal (the boxes are
+ * free for the next frame's refits). */
+int gd_query_group_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b, int n,
+                         const GdConfig* cfgs, void* const* workspaces, const size_t* workspace_bytes,
+                         void* const* host_dst, int max_stats, void* stream, void* traversal_done);
 /* Frame graph: refit A and / or B, then n_queries
- * (<= 8) single-GPU queries (cfgs[i] on workspaces[i]) each followed, when
- * host_dst[i] is not NULL, by the copy of its result record + max_stats
- * GdIterStat into host_dst[i] (pinned) -- captured ONCE as a CUDA graph.
+ * (<= 8) single-GPU queries (cfgs[i] on workspaces[i]; launched as by
+ * gd_query_group_async) each followed, when host_dst[i] is not NULL, by the
+ * copy of its result record + max_stats GdIterStat into host_dst[i]
+ * (pinned) -- captured ONCE as a CUDA graph.
  * gd_frame_graph_launch replays it on `stream` for new rigid transforms of
  * the same meshes (same base vertices; mesh_a / mesh_b carry the frame's
  * rot / trans): one call per frame.  A record with `pending` (a chunked
  * traversal) resumes with gd_query_round as after gd_query_async.  The
- * workspaces and host buffers stay bound to the graph until destroy. */
+ * workspaces and host buffers stay bound to the graph until destroy.
+ * wait_before / traversal_done (cudaEvent_t or NULL): external event nodes
+ * -- every replay first waits for wait_before's latest record, and records
+ * traversal_done once its last traversal has read the trees' boxes.  Two
+ * graphs alternating on two streams, each waiting for the other's
+ * traversal_done, start frame f + 1's refits while frame f's narrow / exact
+ * phases still run. */
 int gd_frame_graph_create(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                           int n_queries, const GdConfig* cfgs, void* const* workspaces,
                           const size_t* workspace_bytes, void* const* host_dst, int max_stats, int refit_a,
-                          int refit_b, void** graph_out);
+                          int refit_b, void* wait_before, void* traversal_done, void** graph_out);
 int gd_frame_graph_launch(void* graph, const GdMesh* mesh_a, const GdMesh* mesh_b, void* stream);
 int gd_frame_graph_destroy(void* graph);
 /* Enqueue the device->host copy of the result record followed by

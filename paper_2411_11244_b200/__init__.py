@@ -24,7 +24,7 @@ _EXPORTS = {
               "SizeGuardError TightnessError TopologyMismatchError",
     "mesh": "RigidTransform TriangleMesh apply_transform load_obj relative_mesh",
     "query": "EngineConfig FrameGraph Front FrontEntry IterationStat PreparedQuery QueryResult QueryState Witness "
-             "adaptive_depth brute_force_max brute_force_min expand_front process_leaf_pair run_dfs_baseline "
+             "adaptive_depth brute_force_max brute_force_min expand_front launch_group process_leaf_pair run_dfs_baseline "
              "run_max_query run_min_query",
     "parallel": "run_sequence run_sequence_minmax run_split_query",
     "scenes": "gen_scene ring_frame_transforms ring_pair_base scene_kinds torus_mesh",

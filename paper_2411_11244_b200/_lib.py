@@ -159,10 +159,13 @@ _SIGNATURES = {
                                     C.POINTER(GdConfig), P, C.c_size_t, C.c_int, C.c_int, P]),
     "gd_query_finish": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
                                   C.POINTER(GdConfig), P, C.c_size_t, P, P]),
+    "gd_query_group_async": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
+                                       C.c_int, C.POINTER(GdConfig), C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                                       C.POINTER(C.c_void_p), C.c_int, P, P]),
     "gd_frame_graph_create": (C.c_int, [C.POINTER(GdMesh), C.POINTER(GdMesh), C.POINTER(GdBvh), C.POINTER(GdBvh),
                                         C.c_int, C.POINTER(GdConfig), C.POINTER(C.c_void_p),
                                         C.POINTER(C.c_size_t), C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
-                                        C.POINTER(C.c_void_p)]),
+                                        P, P, C.POINTER(C.c_void_p)]),
     "gd_frame_graph_launch": (C.c_int, [P, C.POINTER(GdMesh), C.POINTER(GdMesh), P]),
     "gd_frame_graph_destroy": (C.c_int, [P]),
     "gd_query_result_device": (C.c_int, [C.POINTER(GdConfig), P, C.POINTER(C.c_void_p)]),

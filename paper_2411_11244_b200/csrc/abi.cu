@@ -35,9 +35,13 @@ void query_traverse(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const Gd
                     void* ws, size_t ws_bytes, int round, int budget, cudaStream_t s);
 void query_finish(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                   void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s);
+void query_group_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, int n,
+                       const GdConfig* cfgs, void* const* wss, const size_t* ws_bytes, void* const* host_dst,
+                       int max_stats, cudaStream_t s, cudaEvent_t traversal_done, bool external_record);
 void* frame_graph_create(const GdMesh& ma, const GdMesh& mb, const GdBvh& A, const GdBvh& B, int n_queries,
                          const GdConfig* cfgs, void* const* wss, const size_t* ws_bytes, void* const* host_dst,
-                         int max_stats, int refit_a, int refit_b);
+                         int max_stats, int refit_a, int refit_b, cudaEvent_t wait_before,
+                         cudaEvent_t traversal_done);
 void frame_graph_launch(void* h, const GdMesh& ma, const GdMesh& mb, cudaStream_t s);
 void frame_graph_destroy(void* h);
 const void* query_result_device(const GdConfig& cfg, void* ws);
@@ -258,15 +262,26 @@ int gd_query_finish(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, 
   });
 }
 
+int gd_query_group_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b, int n,
+                         const GdConfig* cfgs, void* const* workspaces, const size_t* workspace_bytes,
+                         void* const* host_dst, int max_stats, void* stream, void* traversal_done) {
+  return guarded([&] {
+    GD_CHECK(mesh_a && mesh_b && a && b && cfgs && workspaces && workspace_bytes, GD_ERR_INVALID, "null argument");
+    query_group_async(*mesh_a, *mesh_b, *a, *b, n, cfgs, workspaces, workspace_bytes, host_dst, max_stats,
+                      S(stream), static_cast<cudaEvent_t>(traversal_done), false);
+  });
+}
+
 int gd_frame_graph_create(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                           int n_queries, const GdConfig* cfgs, void* const* workspaces,
                           const size_t* workspace_bytes, void* const* host_dst, int max_stats, int refit_a,
-                          int refit_b, void** graph_out) {
+                          int refit_b, void* wait_before, void* traversal_done, void** graph_out) {
   return guarded([&] {
     GD_CHECK(mesh_a && mesh_b && a && b && graph_out && (n_queries == 0 || (cfgs && workspaces && workspace_bytes)),
              GD_ERR_INVALID, "null argument");
     *graph_out = frame_graph_create(*mesh_a, *mesh_b, *a, *b, n_queries, cfgs, workspaces, workspace_bytes,
-                                    host_dst, max_stats, refit_a, refit_b);
+                                    host_dst, max_stats, refit_a, refit_b, static_cast<cudaEvent_t>(wait_before),
+                                    static_cast<cudaEvent_t>(traversal_done));
   });
 }
 

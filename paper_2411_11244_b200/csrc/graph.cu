@@ -19,6 +19,10 @@ void query_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh
                  void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s, cudaEvent_t traversal_done,
                  int round);
 void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
+void query_group_prepare();
+void query_group_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, int n,
+                       const GdConfig* cfgs, void* const* wss, const size_t* ws_bytes, void* const* host_dst,
+                       int max_stats, cudaStream_t s, cudaEvent_t traversal_done, bool external_record);
 bool is_query_kernel(const void* f);
 void retransform(QArgs& q, const GdMesh& ma, const GdMesh& mb);
 
@@ -35,9 +39,15 @@ struct FrameGraph {
   long long kernels = 0;
 };
 
+// wait_before / traversal_done (cudaEvent_t or null): external event nodes
+// at the graph's start / after its last traversal.  Two graphs alternating
+// on two streams, each waiting for the other's traversal_done, run frame
+// f + 1's refits as soon as frame f's traversals have read the boxes --
+// overlapping frame f's narrow / exact chains (run_sequence_minmax).
 void* frame_graph_create(const GdMesh& ma, const GdMesh& mb, const GdBvh& A, const GdBvh& B, int n_queries,
                          const GdConfig* cfgs, void* const* wss, const size_t* ws_bytes, void* const* host_dst,
-                         int max_stats, int refit_a, int refit_b) {
+                         int max_stats, int refit_a, int refit_b, cudaEvent_t wait_before,
+                         cudaEvent_t traversal_done) {
   GD_CHECK(n_queries >= 0 && n_queries <= 8, GD_ERR_INVALID, "a frame graph holds 0 - 8 queries");
   for (int i = 0; i < n_queries; ++i)
     GD_CHECK(cfgs[i].split_world <= 1 && cfgs[i].n_peers == 0, GD_ERR_CONFIG,
@@ -50,14 +60,19 @@ void* frame_graph_create(const GdMesh& ma, const GdMesh& mb, const GdBvh& A, con
   fg->mb = mb;
   cudaStream_t cap = nullptr;
   try {
+    query_group_prepare();  // the side streams of the narrow chains exist before the capture
     GD_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
     GD_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    if (wait_before) GD_CUDA(cudaStreamWaitEvent(cap, wait_before, cudaEventWaitExternal));
     if (refit_a) refit(ma, A, cap);
     if (refit_b) refit(mb, B, cap);
-    for (int i = 0; i < n_queries; ++i) {
-      query_async(ma, mb, A, B, cfgs[i], wss[i], ws_bytes[i], nullptr, cap, nullptr, 0);
-      if (host_dst && host_dst[i]) query_result_async(cfgs[i], wss[i], host_dst[i], max_stats, cap);
-    }
+    // the traversals back to back, then the queries' narrow / exact chains
+    // side by side (a fork / join in the graph, query.cu query_group_async)
+    if (n_queries > 0)
+      query_group_async(ma, mb, A, B, n_queries, cfgs, wss, ws_bytes, host_dst, max_stats, cap, traversal_done,
+                        true);
+    else if (traversal_done)
+      GD_CUDA(cudaEventRecordWithFlags(traversal_done, cap, cudaEventRecordExternal));
     GD_CUDA(cudaStreamEndCapture(cap, &fg->graph));
     GD_CUDA(cudaStreamDestroy(cap));
     cap = nullptr;

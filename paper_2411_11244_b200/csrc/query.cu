@@ -23,6 +23,7 @@
 #include <chrono>
 #include <cstddef>
 #include <cstring>
+#include <vector>
 
 #include "dfs.cuh"
 
@@ -195,6 +196,39 @@ static void launch_traverse(QArgs q, cudaStream_t s) {
   }
 }
 
+// the narrow / exact chain after a traversal: k_nfilter, k_ntest (min),
+// k_nfilter<rescan>, k_refine.  pdl_first: the first kernel may overlap the
+// drain of the stream's previous kernel (its traversal); off when the chain
+// starts a side stream after an event wait.
+template <bool kMax>
+static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
+  const int sms = num_sms();
+  auto mark = [&](int i) {
+    if (g_profile) GD_CUDA(cudaEventRecord(g_ev[i], s));
+  };
+  // profiling events between the kernels would serialise them: PDL only
+  // when the phases are not being timed
+  if (g_profile) {
+    k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
+    if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
+    mark(3);
+    k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
+    k_refine<kMax><<<refine_grid<kMax>(), kRefineThreads, 0, s>>>(q);  // + witness record in its last block
+  } else {
+    if (pdl_first)
+      launch_pdl(k_nfilter<kMax, false>, sms * 8, 256, s, q);
+    else
+      k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
+    if (!kMax) launch_pdl(k_ntest<kMax>, sms * 4, 256, s, q);
+    launch_pdl(k_nfilter<kMax, true>, sms, 256, s, q);
+    launch_pdl(k_refine<kMax>, refine_grid<kMax>(), kRefineThreads, s, q);
+  }
+  mark(4);
+  mark(5);
+  GD_CUDA(cudaGetLastError());
+  count_launches(kMax ? 3 : 4);
+}
+
 template <bool kMax>
 static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_done) {
   const int sms = num_sms();
@@ -207,24 +241,8 @@ static void launch_query(const QArgs& q, cudaStream_t s, cudaEvent_t traversal_d
   // may start once this event has fired
   if (traversal_done) GD_CUDA(cudaEventRecord(traversal_done, s));
   mark(2);
-  // profiling events between the kernels would serialise them: PDL only
-  // when the phases are not being timed
-  if (g_profile) {
-    k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
-    if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
-    mark(3);
-    k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
-    k_refine<kMax><<<refine_grid<kMax>(), kRefineThreads, 0, s>>>(q);  // + witness record in its last block
-  } else {
-    launch_pdl(k_nfilter<kMax, false>, sms * 8, 256, s, q);
-    if (!kMax) launch_pdl(k_ntest<kMax>, sms * 4, 256, s, q);
-    launch_pdl(k_nfilter<kMax, true>, sms, 256, s, q);
-    launch_pdl(k_refine<kMax>, refine_grid<kMax>(), kRefineThreads, s, q);
-  }
-  mark(4);
-  mark(5);
-  GD_CUDA(cudaGetLastError());
-  count_launches(kMax ? 4 : 5);
+  launch_narrow<kMax>(q, s, true);
+  count_launches(1);
 }
 
 static QArgs make_args(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
@@ -343,6 +361,73 @@ void query_finish(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBv
     launch_query<true>(q, s, nullptr);
   else
     launch_query<false>(q, s, nullptr);
+}
+
+// Several queries on the same trees (config 3: min and max of one frame):
+// their traversals back to back on s -- each needs the whole GPU -- then
+// every query's narrow / exact chain on its own stream, forked after the last
+// traversal and joined back into s.  The chains are short, latency-bound
+// kernels on part of the GPU, so running them side by side hides most of one
+// (and the trees' boxes are free for the next frame's refits once the last
+// traversal is done: `traversal_done`).  Each chain ends with the copy of
+// its result record to host_dst[i] when given.  Streams capture into a
+// graph as a fork / join (frame_graph_create).
+void query_result_async(const GdConfig& cfg, void* ws, void* host_dst, int max_stats, cudaStream_t s);
+struct SideStreams {
+  cudaStream_t st[8] = {};
+  cudaEvent_t fork = nullptr, join[8] = {};
+};
+static SideStreams& side_streams() {
+  static SideStreams ss[kMaxDevices];
+  SideStreams& r = ss[current_device()];
+  if (!r.fork) {
+    for (int i = 0; i < 8; ++i) {
+      GD_CUDA(cudaStreamCreateWithFlags(&r.st[i], cudaStreamNonBlocking));
+      GD_CUDA(cudaEventCreateWithFlags(&r.join[i], cudaEventDisableTiming));
+    }
+    GD_CUDA(cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming));
+  }
+  return r;
+}
+
+void query_group_prepare() { side_streams(); }
+
+void query_group_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, int n,
+                       const GdConfig* cfgs, void* const* wss, const size_t* ws_bytes, void* const* host_dst,
+                       int max_stats, cudaStream_t s, cudaEvent_t traversal_done, bool external_record) {
+  GD_CHECK(n >= 1 && n <= 8, GD_ERR_INVALID, "a query group holds 1 - 8 queries");
+  std::vector<QArgs> qs;
+  for (int i = 0; i < n; ++i) {
+    validate(a, b, cfgs[i]);
+    GD_CHECK(cfgs[i].split_world <= 1, GD_ERR_CONFIG, "query groups hold single-GPU queries");
+    for (int j = 0; j < i; ++j)
+      GD_CHECK(wss[j] != wss[i], GD_ERR_INVALID, "the queries of a group need distinct workspaces");
+    qs.push_back(make_args(ma, mb, a, b, cfgs[i], wss[i], ws_bytes[i], nullptr));
+  }
+  for (int i = 0; i < n; ++i) {
+    if (cfgs[i].kind == 1)
+      launch_traverse<true>(qs[i], s);
+    else
+      launch_traverse<false>(qs[i], s);
+  }
+  count_launches(n);
+  if (traversal_done)  // (an external event node when captured for another graph to wait on)
+    GD_CUDA(cudaEventRecordWithFlags(traversal_done, s, external_record ? cudaEventRecordExternal : 0));
+  SideStreams& ss = side_streams();
+  if (n > 1) GD_CUDA(cudaEventRecord(ss.fork, s));
+  for (int i = 0; i < n; ++i) {
+    cudaStream_t si = i == 0 ? s : ss.st[i - 1];
+    if (i > 0) GD_CUDA(cudaStreamWaitEvent(si, ss.fork, 0));
+    if (cfgs[i].kind == 1)
+      launch_narrow<true>(qs[i], si, i == 0);
+    else
+      launch_narrow<false>(qs[i], si, i == 0);
+    if (host_dst && host_dst[i]) query_result_async(cfgs[i], wss[i], host_dst[i], max_stats, si);
+    if (i > 0) {
+      GD_CUDA(cudaEventRecord(ss.join[i - 1], si));
+      GD_CUDA(cudaStreamWaitEvent(s, ss.join[i - 1], 0));
+    }
+  }
 }
 
 static_assert(offsetof(QState, stats) == offsetof(QState, res) + sizeof(GdResult),

@@ -97,13 +97,18 @@ def run_sequence_minmax(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kinds=("min", 
                         group=None) -> dict:
     """Config 3: every kind in `kinds` (min and max distance) at every frame
     of a rigid-motion sequence, frames sharded over the ranks like
-    run_sequence.  Each frame -- refit A, refit B, the queries and the copies
-    of their records -- is ONE CUDA graph replay (query.FrameGraph); two
-    graphs alternate, so the host reads frame f's records while frame f + 1
-    runs.  Returns {kind: (n_frames, 3) array of (distance, tri_a, tri_b)}
-    on every rank."""
+    run_sequence.  Each frame -- refit A, refit B, the queries (traversals
+    back to back, then their narrow / exact chains side by side) and the
+    copies of their records -- is ONE CUDA graph replay (query.FrameGraph).
+    Two graphs alternate on two streams, each replay waiting (on the device)
+    for the previous frame's traversals only: frame f + 1's refits overlap
+    frame f's narrow / exact phases, and the host reads frame f's records
+    while frame f + 1 runs.  Returns {kind: (n_frames, 3) array of
+    (distance, tri_a, tri_b)} on every rank."""
+    import torch
+
     from .mesh import apply_transform
-    from .query import FrameGraph
+    from .query import FrameGraph, run_max_query, run_min_query
 
     rank, world = world_info(group)
     mine = list(frames_of_rank(len(transforms), rank, world))
@@ -115,31 +120,58 @@ def run_sequence_minmax(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kinds=("min", 
                 mesh_b if xb is None else apply_transform(mesh_b, xb))
 
     def take(f, g):
-        for k, r in g.results().items():
+        res = g.results()
+        if any(r is None for r in res.values()):
+            # a chunked traversal (front larger than the arena) whose later
+            # rounds would read boxes the next frame may have refit already:
+            # wait for everything in flight, then this frame on its own
+            torch.cuda.synchronize()
+            a, b = moved(f)
+            from .bvh import refit
+
+            refit(bvh_a, a)
+            refit(bvh_b, b)
+            res = {k: (run_min_query if k == "min" else run_max_query)(a, b, bvh_a, bvh_b, cfg) for k in kinds}
+            torch.cuda.synchronize()  # before the graphs' streams touch the boxes again
+        for k, r in res.items():
             w = r.witness
             local[k][f] = (r.distance, -1 if w is None else w.tri_a, -1 if w is None else w.tri_b)
 
-    # the two graphs are kept for the next call on the same trees / meshes
+    # the two graphs (with their events and streams) are kept for the next
+    # call on the same trees / meshes
     key = (id(bvh_a), id(bvh_b), id(mesh_a._root), id(mesh_b._root), tuple(kinds), cfg)
     ent = _FRAME_GRAPHS.get(key)
     if ent is None or ent[0] is not bvh_a or ent[1] is not bvh_b:
-        if ent is not None:
-            for g in ent[2]:
-                g.close()
-        ent = (bvh_a, bvh_b, [])
-        _FRAME_GRAPHS.clear()  # one sequence's graphs at a time (each holds two query workspaces)
+        release_frame_graphs()  # one sequence's graphs at a time (each holds its query workspaces)
+        events = (torch.cuda.Event(), torch.cuda.Event())
+        for e in events:
+            e.record()  # a first replay's wait is then satisfied at once
+        ent = (bvh_a, bvh_b, [], events, (torch.cuda.Stream(), torch.cuda.Stream()))
         _FRAME_GRAPHS[key] = ent
-    graphs, pending = ent[2], None
+    graphs, events, streams = ent[2], ent[3], ent[4]
+    if not mine:
+        return {k: gather_frames(len(transforms), local[k], group) for k in kinds}
+    # both graphs exist before any replay: creating one stages / refits on
+    # the current stream, which must not race a replay on the side streams
+    while len(graphs) < 2:
+        j = len(graphs)
+        a, b = moved(mine[0])
+        graphs.append(FrameGraph(a, b, bvh_a, bvh_b, kinds, cfg, wait_event=events[1 - j], done_event=events[j]))
+    cur = torch.cuda.current_stream()
+    for st in streams:
+        st.wait_stream(cur)  # after the caller's work (builds, refits, earlier frames)
+    pending = None
     for i, f in enumerate(mine):
         a, b = moved(f)
-        if len(graphs) < 2:
-            graphs.append(FrameGraph(a, b, bvh_a, bvh_b, kinds, cfg))
-        g = graphs[i % 2].launch(a, b)
+        j = i % 2
+        g = graphs[j].launch(a, b, stream=streams[j])
         if pending is not None:
             take(*pending)
         pending = (f, g)
     if pending is not None:
         take(*pending)
+    for st in streams:
+        cur.wait_stream(st)
     return {k: gather_frames(len(transforms), local[k], group) for k in kinds}
 
 
@@ -150,6 +182,8 @@ def release_frame_graphs():
     """Destroy the cached frame graphs of run_sequence_minmax (and their
     query workspaces)."""
     for ent in _FRAME_GRAPHS.values():
+        for st in ent[4]:
+            st.synchronize()  # a replay may still be in flight
         for g in ent[2]:
             g.close()
     _FRAME_GRAPHS.clear()

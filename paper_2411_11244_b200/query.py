@@ -482,16 +482,56 @@ class PreparedQuery:
         return _result(self.kind, r, stats)
 
 
+def launch_group(plans, stream=None, traversal_done=None, host_dst=None, max_stats: int = 0):
+    """Enqueue several PreparedQuery plans on the same meshes and trees (the
+    min and max query of one frame, config 3) as one group
+    (gd_query_group_async): their traversals back to back, then their narrow
+    / exact chains side by side on forked streams, joined back into `stream`.
+    Each plan's record is read with collect() as after launch(); with
+    `host_dst` (pinned buffers, one per plan) the records are also copied at
+    the end of each chain.  `traversal_done` (a torch.cuda.Event) is recorded
+    after the last traversal."""
+    plans = list(plans)
+    if not plans:
+        raise ValueError("launch_group needs at least one query")
+    p0 = plans[0]
+    for p in plans[1:]:
+        if (p.g_a.box, p.g_b.box, p.g_ma.vtx, p.g_mb.vtx) != (p0.g_a.box, p0.g_b.box, p0.g_ma.vtx, p0.g_mb.vtx) or \
+                bytes(p.g_ma) != bytes(p0.g_ma) or bytes(p.g_mb) != bytes(p0.g_mb):
+            raise ValueError("the queries of a group share their meshes, transforms and trees")
+    n = len(plans)
+    cfgs = (_lib.GdConfig * n)(*[p.g_cfg for p in plans])
+    wss = (C.c_void_p * n)(*[p.ws.data_ptr() for p in plans])
+    sizes = (C.c_size_t * n)(*[p.ws.numel() for p in plans])
+    dst = None if host_dst is None else (C.c_void_p * n)(*[t.data_ptr() for t in host_dst])
+    ev = None
+    if traversal_done is not None:
+        if not traversal_done.cuda_event:
+            traversal_done.record()
+        ev = C.c_void_p(traversal_done.cuda_event)
+    _lib.check(_lib.lib().gd_query_group_async(C.byref(p0.g_ma), C.byref(p0.g_mb), C.byref(p0.g_a),
+                                               C.byref(p0.g_b), n, cfgs, wss, sizes, dst, int(max_stats),
+                                               stream or _lib.stream_ptr(), ev), "query_group")
+
+
 class FrameGraph:
     """One frame of a rigid-motion sequence -- refit both trees, then one
     query per kind in `kinds` with the copy of each result record to pinned
     host memory -- captured once as a CUDA graph (gd_frame_graph_create,
     SURVEY.md 8(f) row 1) and replayed per frame for the frame's moved
     meshes (same base meshes, any rigid transforms): one host call per frame.
-    The queries use private workspaces bound to the graph.  Single GPU
-    (no split query)."""
+    The queries use private workspaces bound to the graph; their traversals
+    run back to back, then their narrow / exact chains side by side
+    (gd_query_group_async).  Single GPU (no split query).
 
-    def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, kinds=("min", "max"), cfg: EngineConfig | None = None):
+    wait_event / done_event (torch.cuda.Event): every replay first waits for
+    wait_event's latest record and records done_event once its traversals
+    have read the trees' boxes -- two graphs alternating on two streams, each
+    waiting for the other's done_event, run frame f + 1's refits while frame
+    f's narrow / exact phases still run (run_sequence_minmax)."""
+
+    def __init__(self, mesh_a, mesh_b, bvh_a, bvh_b, kinds=("min", "max"), cfg: EngineConfig | None = None,
+                 wait_event=None, done_event=None):
         torch = _lib.torch()
         cfg = cfg or EngineConfig()
         if not kinds or any(k not in ("min", "max") for k in kinds):
@@ -511,21 +551,33 @@ class FrameGraph:
         sizes = (C.c_size_t * n)(*[p.ws.numel() for p in self.plans])
         dst = (C.c_void_p * n)(*[t.data_ptr() for t in self._pinned])
         g_ma, g_mb = mesh_a.device_view(), mesh_b.device_view()
+
+        def handle(ev):
+            if ev is None:
+                return None
+            if not ev.cuda_event:  # torch creates the event lazily
+                ev.record()
+            return C.c_void_p(ev.cuda_event)
+
+        self.overlapped = wait_event is not None
         h = C.c_void_p()
         _lib.check(_lib.lib().gd_frame_graph_create(C.byref(g_ma), C.byref(g_mb), C.byref(bvh_a.device_view()),
                                                     C.byref(bvh_b.device_view()), n, cfgs, wss, sizes, dst,
-                                                    _MAX_STATS, 1, 1, C.byref(h)), "frame_graph_create")
+                                                    _MAX_STATS, 1, 1, handle(wait_event), handle(done_event),
+                                                    C.byref(h)), "frame_graph_create")
         self._h = h
         self._ready = torch.cuda.Event()
 
     def launch(self, mesh_a, mesh_b, stream=None):
         """Enqueue the frame for `mesh_a` / `mesh_b` (rigid moves of the
-        captured meshes' bases)."""
+        captured meshes' bases) on `stream` (a torch.cuda.Stream; default:
+        the current stream)."""
         if (mesh_a._root, mesh_b._root) != self._roots:
             raise ValueError("a FrameGraph replays moves of the meshes it was captured with")
         g_ma, g_mb = mesh_a.device_view(), mesh_b.device_view()
         _lib.check(_lib.lib().gd_frame_graph_launch(self._h, C.byref(g_ma), C.byref(g_mb),
-                                                    stream or _lib.stream_ptr()), "frame_graph_launch")
+                                                    stream.cuda_stream if stream is not None else _lib.stream_ptr()),
+                   "frame_graph_launch")
         for bvh, m in zip(self.trees, (mesh_a, mesh_b)):
             bvh._mesh = m  # the boxes now describe the moved mesh
             bvh._export_cache = None
@@ -533,7 +585,7 @@ class FrameGraph:
         for p in self.plans:
             p.meshes = (mesh_a, mesh_b)
             p.g_ma, p.g_mb = g_ma, g_mb
-        self._ready.record()
+        self._ready.record(stream)
         return self
 
     def results(self) -> dict:
@@ -545,6 +597,12 @@ class FrameGraph:
             r = _lib.GdResult.from_address(base)
             stats = (_lib.GdIterStat * _MAX_STATS).from_address(base + C.sizeof(_lib.GdResult))
             if r.pending and r.status == 0:  # a chunked traversal: the remaining rounds, synchronously
+                if self.overlapped:
+                    # the next frame's refits may already have rewritten the
+                    # boxes the remaining rounds would read: the caller
+                    # recomputes this frame (run_sequence_minmax)
+                    out[kind] = None
+                    continue
                 p._finish_rounds(r, _lib.stream_ptr())
                 out[kind] = _result(kind, p.res, p.stats)
             else:

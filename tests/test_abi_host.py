@@ -28,7 +28,7 @@ def test_library_exports_header(md):
     for name in declared:
         assert hasattr(lib, name), name
     assert sorted(_lib.exported_symbols()) == declared
-    assert lib.gd_abi_version() == 14
+    assert lib.gd_abi_version() == 15
     assert b"sm_100a" in lib.gd_version()
 
 

@@ -518,3 +518,33 @@ def test_nonfinite_vertices(md, gpu, oracle, prec):
         assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (ia, ib)
         r = md.run_max_query(a2, b, ta, tb, cfg)
         assert r.distance == np.inf and r.witness is None
+
+
+@pytest.mark.parametrize("scene", ["interlocked-rings", "nested-shells"])
+def test_query_group_matches_separate(md, gpu, scene):
+    """launch_group (gd_query_group_async: the min and max traversals back to
+    back, then both narrow / exact chains side by side on forked streams)
+    gives each query's separate answer -- distance, witness, points --
+    including when the group is replayed with the other order
+    and when one plan appears alone."""
+    params = {"nu": 60, "nv": 30} if scene == "interlocked-rings" else {}
+    a, b = md.gen_scene(scene, params)
+    xa = md.RigidTransform.from_axis_angle([0.3, 1.0, 0.2], 0.7, [0.05, -0.02, 0.01])
+    a = md.apply_transform(a, xa)
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    cfg = md.EngineConfig(front_hard_cap=1 << 30)
+    want = {k: (md.run_min_query if k == "min" else md.run_max_query)(a, b, ta, tb, cfg) for k in ("min", "max")}
+    plans = {k: md.PreparedQuery(a, b, ta, tb, cfg, k, private_workspace=True) for k in ("min", "max")}
+    for order in (("min", "max"), ("max", "min"), ("min",), ("max",)):
+        md.launch_group([plans[k] for k in order])
+        for k in order:
+            got = plans[k].collect()
+            w = want[k]
+            assert got.distance == w.distance, (order, k)
+            assert (got.witness.tri_a, got.witness.tri_b) == (w.witness.tri_a, w.witness.tri_b), (order, k)
+            np.testing.assert_array_equal(got.witness.point_a, w.witness.point_a)
+            np.testing.assert_array_equal(got.witness.point_b, w.witness.point_b)
+            assert got.iterations and got.iterations[-1].front_out == 0, (order, k)
+    with pytest.raises(ValueError, match="share"):
+        other = md.PreparedQuery(b, a, tb, ta, cfg, "min", private_workspace=True)
+        md.launch_group([plans["min"], other])
