@@ -143,3 +143,29 @@ def test_arena_too_small_fails_loudly(md, gpu):
 def test_arena_config_validation(md):
     with pytest.raises(md.ConfigError):
         md.EngineConfig(arena_entries=-1)
+
+
+def test_sequence_minmax_chunked_frames(md, gpu):
+    """run_sequence_minmax overlaps frame f + 1's refits with frame f's narrow
+    phases; a frame whose traversal is chunked (the arena far too small)
+    cannot resume its later rounds after the next frame's refit, so it is
+    recomputed through the plain API -- every frame equals the plain API's
+    min and max, with a roomy arena and with a tiny one."""
+    from paper_2411_11244_b200.parallel import release_frame_graphs
+
+    a0, b0 = md.ring_pair_base(120, 60)
+    ta, tb = md.build_f12(a0), md.build_f12(b0)
+    xfs = [md.ring_frame_transforms(f) for f in range(0, 70, 7)]
+    want = []
+    for xa, xb in xfs:
+        a, b = md.apply_transform(a0, xa), md.apply_transform(b0, xb)
+        cfg = md.EngineConfig(front_hard_cap=1 << 30)
+        want.append((md.run_min_query(a, b, ta, tb, cfg), md.run_max_query(a, b, ta, tb, cfg)))
+    for arena in (0, 1 << 10):
+        cfg = md.EngineConfig(front_hard_cap=1 << 30, arena_entries=arena)
+        out = md.run_sequence_minmax(a0, b0, ta, tb, xfs, ("min", "max"), cfg)
+        release_frame_graphs()
+        for f, (wmin, wmax) in enumerate(want):
+            for k, w in (("min", wmin), ("max", wmax)):
+                d, t1, t2 = out[k][f]
+                assert d == w.distance and (int(t1), int(t2)) == (w.witness.tri_a, w.witness.tri_b), (arena, f, k)
