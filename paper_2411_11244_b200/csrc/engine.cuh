@@ -261,23 +261,28 @@ __device__ __forceinline__ double xf_row(const double* r, double x, double y, do
   if (order == 2) return __fma_rn(r[0], x, __fma_rn(r[1], y, __dmul_rn(r[2], z)));
   return __fma_rn(r[2], z, __fma_rn(r[1], y, __dmul_rn(r[0], x)));
 }
+// kOrder >= 0: the order fixed at compile time (the exact pass is
+// instantiated per order: a runtime switch per vertex cost it ~4 us on the
+// rings); -1: GdMesh.xf_order at run time
+template <int kOrder = -1>
 __device__ __forceinline__ V3<double> mesh_vertex(const GdMesh& m, long long i) {
   const double* p = m.vtx + 3 * i;
   double x = p[0], y = p[1], z = p[2];
   if (!m.has_xf) return {x, y, z};
   const double* R = m.rot;
-  return {__dadd_rn(xf_row(R, x, y, z, m.xf_order), m.trans[0]),
-          __dadd_rn(xf_row(R + 3, x, y, z, m.xf_order), m.trans[1]),
-          __dadd_rn(xf_row(R + 6, x, y, z, m.xf_order), m.trans[2])};
+  const int o = kOrder >= 0 ? kOrder : m.xf_order;
+  return {__dadd_rn(xf_row(R, x, y, z, o), m.trans[0]),
+          __dadd_rn(xf_row(R + 3, x, y, z, o), m.trans[1]),
+          __dadd_rn(xf_row(R + 6, x, y, z, o), m.trans[2])};
 }
 
-template <typename T>
+template <typename T, int kOrder = -1>
 __device__ __forceinline__ Tri<T> mesh_tri(const GdMesh& m, long long t) {
   const int32_t* ix = m.tri + 3 * t;
   Tri<T> r;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    V3<double> v = mesh_vertex(m, ix[c]);
+    V3<double> v = mesh_vertex<kOrder>(m, ix[c]);
     r.v[c] = {T(v.x), T(v.y), T(v.z)};  // cast-then-gather (mesh.py:64-66)
   }
   return r;

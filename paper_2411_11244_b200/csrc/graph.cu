@@ -120,6 +120,8 @@ void frame_graph_launch(void* h, const GdMesh& ma, const GdMesh& mb, cudaStream_
   GD_CHECK(current_device() == fg->dev, GD_ERR_INVALID, "frame graph launched on another device");
   GD_CHECK(ma.vtx == fg->ma.vtx && mb.vtx == fg->mb.vtx && ma.nv == fg->ma.nv && mb.nv == fg->mb.nv,
            GD_ERR_TOPOLOGY, "a frame graph replays the meshes it was captured with (same base vertices), moved");
+  GD_CHECK(ma.xf_order == fg->ma.xf_order && mb.xf_order == fg->mb.xf_order, GD_ERR_INVALID,
+           "a frame graph's exact pass is instantiated for the captured meshes' transform order (xf_order)");
   const XfF32 xa = xf32_host(ma), xb = xf32_host(mb);
   for (size_t i = 0; i < fg->refit_nodes.size(); ++i) {
     cudaKernelNodeParams p = fg->refit_params[i];

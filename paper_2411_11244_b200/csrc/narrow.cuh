@@ -11,16 +11,16 @@ namespace gd {
 // exact narrow phase for one triangle pair -> 128-bit key (distance bits,
 // tri_a, tri_b): its minimum is the reference's lexicographic witness rule
 // (query.py:205-220, 299)
-template <bool kMax>
+template <bool kMax, int kOrder = -1>
 __device__ __forceinline__ Key128 exact_key(const QArgs& q, unsigned ta, unsigned tb) {
   double d;
   if (q.cfg.precision == 32) {
-    Tri<float> a = mesh_tri<float>(q.ma, ta), b = mesh_tri<float>(q.mb, tb);
+    Tri<float> a = mesh_tri<float, kOrder>(q.ma, ta), b = mesh_tri<float, kOrder>(q.mb, tb);
     float d2 = kMax ? tri_tri_max_d2<Exact<float>, float, false>(a, b, nullptr, nullptr)
                     : tri_tri_min_d2_lean<Exact<float>, float>(a, b);
     d = (double)__fsqrt_rn(d2);
   } else {
-    Tri<double> a = mesh_tri<double>(q.ma, ta), b = mesh_tri<double>(q.mb, tb);
+    Tri<double> a = mesh_tri<double, kOrder>(q.ma, ta), b = mesh_tri<double, kOrder>(q.mb, tb);
     double d2 = kMax ? tri_tri_max_d2<Exact<double>, double, false>(a, b, nullptr, nullptr)
                      : tri_tri_min_d2_lean<Exact<double>, double>(a, b);
     d = __dsqrt_rn(d2);
@@ -346,7 +346,10 @@ __device__ void finalize(const QArgs& q);
 // cost one load each and no compaction pass is needed.
 constexpr int kRefineThreads = 64;
 
-template <bool kMax>
+// kOrder: the float64 transform's operation order of both meshes
+// (GdMesh.xf_order, fixed per process), -1 = read at run time (meshes with
+// different orders)
+template <bool kMax, int kOrder>
 // min: the lean float64 feature loop keeps ~150 registers live (no spills at
 // 4 blocks / SM: 41 -> 36 us on the rings); max is short and stays at 12
 __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : 4) void k_refine(QArgs q) {
@@ -367,7 +370,7 @@ __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : 4) void k_refine(QArgs 
     const float f = q.band_d[j];
     const uint2 ids = q.band_ids[j];  // loaded with f: no second dependent round trip
     if (!(kMax ? f >= fb - E : f <= fb + E)) continue;  // +-inf (warm pair) always passes
-    const Key128 k = exact_key<kMax>(q, ids.x, ids.y);
+    const Key128 k = exact_key<kMax, kOrder>(q, ids.x, ids.y);
     if (key_less(k, best)) best = k;
     ++evals;
   }

@@ -145,16 +145,41 @@ static void launch_pdl(void (*kernel)(Args...), unsigned grid, unsigned block, c
 // k_refine runs as a resident grid (blocks per SM x SMs) striding over the
 // band: a few hundred blocks for a rings band of ~20K entries instead of
 // thousands of mostly idle ones (each also takes a turn on the done counter)
-template <bool kMax>
+template <bool kMax, int kOrder>
 static unsigned refine_grid() {
   static unsigned g[kMaxDevices] = {0};
   const int dev = current_device();
   if (g[dev] == 0) {
     int per_sm = 0;
-    GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine<kMax>, kRefineThreads, 0));
+    GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine<kMax, kOrder>, kRefineThreads, 0));
     g[dev] = (unsigned)(std::max(per_sm, 1) * num_sms());
   }
   return g[dev];
+}
+// the exact pass instantiated for the meshes' transform order (engine.cuh
+// mesh_vertex): both meshes' order when they agree (always, within one
+// process), else the run-time switch
+static int exact_order(const QArgs& q) {
+  const int oa = q.ma.xf_order, ob = q.mb.xf_order;
+  return oa == ob && oa >= 0 && oa <= 2 ? oa : -1;
+}
+template <bool kMax>
+static void launch_refine(const QArgs& q, cudaStream_t s, bool pdl) {
+  switch (exact_order(q)) {
+#define GD_REFINE(O)                                                                     \
+  case O:                                                                                \
+    if (pdl)                                                                             \
+      launch_pdl(k_refine<kMax, O>, refine_grid<kMax, O>(), kRefineThreads, s, q);        \
+    else                                                                                 \
+      k_refine<kMax, O><<<refine_grid<kMax, O>(), kRefineThreads, 0, s>>>(q);             \
+    break;
+    GD_REFINE(0)
+    GD_REFINE(1)
+    GD_REFINE(2)
+    default:
+      GD_REFINE(-1)
+#undef GD_REFINE
+  }
 }
 
 // k_traverse launch epochs: unique per launch within the process (odd,
@@ -213,7 +238,7 @@ static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
     if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
     mark(3);
     k_nfilter<kMax, true><<<sms, 256, 0, s>>>(q);  // exits at once unless the band overflowed (rare: small grid)
-    k_refine<kMax><<<refine_grid<kMax>(), kRefineThreads, 0, s>>>(q);  // + witness record in its last block
+    launch_refine<kMax>(q, s, false);  // + witness record in its last block
   } else {
     if (pdl_first)
       launch_pdl(k_nfilter<kMax, false>, sms * 8, 256, s, q);
@@ -221,7 +246,7 @@ static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
       k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
     if (!kMax) launch_pdl(k_ntest<kMax>, sms * 4, 256, s, q);
     launch_pdl(k_nfilter<kMax, true>, sms, 256, s, q);
-    launch_pdl(k_refine<kMax>, refine_grid<kMax>(), kRefineThreads, s, q);
+    launch_refine<kMax>(q, s, true);
   }
   mark(4);
   mark(5);
@@ -289,8 +314,11 @@ bool is_query_kernel(const void* f) {
                       (const void*)k_traverse_min_split,   (const void*)k_traverse_max_split,
                       (const void*)k_nfilter<false, false>, (const void*)k_nfilter<false, true>,
                       (const void*)k_nfilter<true, false>,  (const void*)k_nfilter<true, true>,
-                      (const void*)k_ntest<false>,          (const void*)k_refine<false>,
-                      (const void*)k_refine<true>};
+                      (const void*)k_ntest<false>,
+                      (const void*)k_refine<false, 0>,      (const void*)k_refine<true, 0>,
+                      (const void*)k_refine<false, 1>,      (const void*)k_refine<true, 1>,
+                      (const void*)k_refine<false, 2>,      (const void*)k_refine<true, 2>,
+                      (const void*)k_refine<false, -1>,     (const void*)k_refine<true, -1>};
   for (const void* k : ks)
     if (k == f) return true;
   return false;
@@ -488,7 +516,7 @@ static void launch_dfs(const QArgs& q, cudaStream_t s) {
   const long long m = q.ma.m;
   if (m > 0) k_dfs<kMax><<<(unsigned)((m + kDfsThreads - 1) / kDfsThreads), kDfsThreads, 0, s>>>(q);
   k_dfs_check<<<1, 1, 0, s>>>(q.S);
-  k_refine<kMax><<<refine_grid<kMax>(), kRefineThreads, 0, s>>>(q);
+  launch_refine<kMax>(q, s, false);
   GD_CUDA(cudaGetLastError());
   count_launches(m > 0 ? 5 : 4);
 }

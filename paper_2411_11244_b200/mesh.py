@@ -195,6 +195,10 @@ class TriangleMesh:
         g.tri = tr.data_ptr()
         g.nv = vt.shape[0]
         g.m = tr.shape[0]
+        # the host BLAS's transform order, also on unmoved meshes: the exact
+        # pass is instantiated per order (a frame graph captured with an
+        # unmoved mesh replays moved ones)
+        g.xf_order = blas_order()
         if self._rot is None:
             g.rot[:] = [1.0, 0.0, 0.0, 0.0, 1.0, 0.0, 0.0, 0.0, 1.0]
             g.trans[:] = [0.0, 0.0, 0.0]
@@ -203,7 +207,6 @@ class TriangleMesh:
             g.rot[:] = [float(x) for x in self._rot.reshape(9)]
             g.trans[:] = [float(x) for x in self._trans.reshape(3)]
             g.has_xf = 1
-            g.xf_order = blas_order()
         self._gview = g
         return g
 

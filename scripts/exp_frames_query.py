@@ -1,6 +1,6 @@
 """Per-frame device time of the rings min query (CUDA events around each
-launch, refits outside the region) over the bench's frames, plus the mean of
-back-to-back launches of one frame: python scripts/exp_frames_query.py [f0 f1]"""
+launch, refits outside the region) over the bench's frames:
+python scripts/exp_frames_query.py [f0 f1 [kind]]"""
 import sys
 from pathlib import Path
 
@@ -11,6 +11,7 @@ import torch  # noqa: E402
 import paper_2411_11244_b200 as md  # noqa: E402
 
 f0, f1 = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (3, 23)
+kind = sys.argv[3] if len(sys.argv) > 3 else "min"
 tz, tb = md.ring_pair_base(2500, 1500)
 A, B = md.build_f12(tz), md.build_f12(tb)
 cfg = md.EngineConfig(front_hard_cap=1 << 27)
@@ -21,7 +22,7 @@ for f in range(f0, f1):
     a, b = md.apply_transform(tz, xa), md.apply_transform(tb, xb)
     md.refit(A, a)
     md.refit(B, b)
-    pq = md.PreparedQuery(a, b, A, B, cfg, "min")
+    pq = md.PreparedQuery(a, b, A, B, cfg, kind)
     pq.run()
     torch.cuda.synchronize()
     t = []
@@ -32,5 +33,5 @@ for f in range(f0, f1):
         torch.cuda.synchronize()
         t.append(ev[0].elapsed_time(ev[1]))
     ms.append(float(np.median(t)))
-print("per-frame query ms", np.round(ms, 4).tolist())
-print("mean", round(float(np.mean(ms)), 4), "min", round(float(np.min(ms)), 4))
+print(kind, "per-frame query ms", np.round(ms, 4).tolist())
+print(kind, "mean", round(float(np.mean(ms)), 4), "min", round(float(np.min(ms)), 4))

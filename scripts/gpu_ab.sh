@@ -8,7 +8,9 @@ if [[ -z $NOTESTS ]]; then
   tail -3 gpurun_out/pytest_gpu.log
 fi
 for v in ${VARIANTS:-libgdist.so}; do
-  echo "$v production per-frame:"; GDIST_LIB_VARIANT=$v timeout 300 python scripts/exp_frames_query.py | tail -1
+  for kind in ${KINDS:-min}; do
+    echo "$v production per-frame:"; GDIST_LIB_VARIANT=$v timeout 300 python scripts/exp_frames_query.py 3 23 $kind | tail -1
+  done
   [[ -n $NOANATOMY ]] && continue
   for kind in min max; do
     GDIST_LIB_VARIANT=$v timeout 300 python scripts/exp_query.py 2500 1500 7 $kind > gpurun_out/ab_${v%.so}_$kind.log 2>&1
