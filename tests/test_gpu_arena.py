@@ -169,3 +169,22 @@ def test_sequence_minmax_chunked_frames(md, gpu):
             for k, w in (("min", wmin), ("max", wmax)):
                 d, t1, t2 = out[k][f]
                 assert d == w.distance and (int(t1), int(t2)) == (w.witness.tri_a, w.witness.tri_b), (arena, f, k)
+
+
+def test_back_to_back_launches_one_workspace(md, gpu):
+    """Many queries enqueued back to back on one workspace without a host
+    sync: every k_traverse launch meets on its own launch epoch (no memset,
+    traverse.cu prologue_barrier), so a launch never starts from the previous
+    one's state -- all answers equal the first (a duplicated epoch would
+    deadlock or, with the spin watchdog, fail loudly)."""
+    a, b = _scene(md, "rings")
+    ta, tb = _trees(md, a, b)
+    cfg = md.EngineConfig(front_hard_cap=1 << 30)
+    for kind in ("min", "max"):
+        pq = md.PreparedQuery(a, b, ta, tb, cfg, kind)
+        want = pq.run()
+        for _ in range(64):
+            pq.launch()
+        got = pq.collect()
+        assert got.distance == want.distance and got.witness.tri_a == want.witness.tri_a, kind
+        assert got.witness.tri_b == want.witness.tri_b, kind
