@@ -12,7 +12,10 @@ namespace gd {
 #define GD_EXPAND_THREADS 512
 #endif
 constexpr int kExpandThreads = GD_EXPAND_THREADS;
-constexpr int kK1Rounds = 4;                                       // entries / thread / tile (k == 1)
+#ifndef GD_K1_ROUNDS
+#define GD_K1_ROUNDS 4
+#endif
+constexpr int kK1Rounds = GD_K1_ROUNDS;                            // entries / thread / tile (k == 1)
 constexpr int kK1Tile = kExpandThreads * kK1Rounds;
 constexpr int kK1Stage = kK1Tile * 4;                              // staged survivors (<= 4 / entry)
 // device schedule default (GdConfig.schedule == 0): fronts up to this many
