@@ -405,8 +405,10 @@ struct SideStreams {
   cudaStream_t st[8] = {};
   cudaEvent_t fork = nullptr, join[8] = {};
 };
+// per host thread (and device): two threads launching groups at once never
+// share the fork / join events
 static SideStreams& side_streams() {
-  static SideStreams ss[kMaxDevices];
+  static thread_local SideStreams ss[kMaxDevices];
   SideStreams& r = ss[current_device()];
   if (!r.fork) {
     for (int i = 0; i < 8; ++i) {
