@@ -125,3 +125,42 @@ def test_concurrent_host_threads(md, gpu):
     for t in threads:
         t.join()
     assert not errors, errors[:5]
+
+
+def test_concurrent_query_groups(md, gpu):
+    """Query groups (gd_query_group_async: forked narrow chains) launched from
+    several host threads at once on their own streams: each thread's fork /
+    join events are its own, every group returns its scene's answers."""
+    import torch
+
+    scenes = []
+    for seed in range(4):
+        a, b = md.gen_scene("random-blobs", {"n": 300, "seed": 10 + seed, "gap": 0.05})
+        ta, tb = md.build_f12(a), md.build_f12(b)
+        want = {k: (md.run_min_query if k == "min" else md.run_max_query)(a, b, ta, tb) for k in ("min", "max")}
+        scenes.append((a, b, ta, tb, want))
+    errors = []
+
+    def work(i):
+        torch.cuda.set_device(0)
+        a, b, ta, tb, want = scenes[i]
+        try:
+            plans = [md.PreparedQuery(a, b, ta, tb, md.EngineConfig(), k, private_workspace=True)
+                     for k in ("min", "max")]
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                for rep in range(20):
+                    md.launch_group(plans)
+                    for k, p in zip(("min", "max"), plans):
+                        r = p.collect()
+                        if r.distance != want[k].distance or r.witness.tri_a != want[k].witness.tri_a:
+                            errors.append((i, rep, k, r.distance, want[k].distance))
+        except Exception as exc:  # report, never hide
+            errors.append((i, repr(exc)))
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(scenes))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:5]
