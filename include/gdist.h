@@ -195,8 +195,11 @@ typedef struct GdResult {
   int32_t iterations;
   int32_t status;
   int32_t rounds;            /* traversal rounds (one per leaf chunk)          */
-  int32_t pending;           /* nonzero: levels remain -- the caller runs another
-                              * round (gd_query_round); gd_query / collect do */
+  int32_t pending;           /* nonzero: not final -- the caller runs
+                              * gd_query_round(round = rounds) until it is 0
+                              * (gd_query / collect do): bit 0 levels remain
+                              * (another traversal round), bit 1 the band
+                              * overflowed (the rescan pass runs first) */
 } GdResult;
 
 /* IterationStat (query.py:147-162). */
@@ -286,9 +289,11 @@ int gd_query_async(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, c
                    const GdConfig* cfg, void* workspace, size_t workspace_bytes,
                    GdResult* result_dev, void* stream);
 /* Resume a query whose record (gd_query_collect / gd_query_result_async)
- * has `pending` set: enqueue traversal round `round` (1, 2, ...: one more
- * than the record's `rounds`) with its narrow and exact phases on the same
- * workspace; the record is rewritten at its end.  gd_query loops itself. */
+ * has `pending` set, with round = the record's `rounds`: if the round's band
+ * overflowed (pending bit 1) the rescan pass and the exact pass again, else
+ * traversal round `round` with its narrow and exact phases, on the same
+ * workspace; the record is rewritten at its end.  Reads two flags of the
+ * workspace (a short synchronisation of `stream`).  gd_query loops itself. */
 int gd_query_round(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const GdBvh* b,
                    const GdConfig* cfg, void* workspace, size_t workspace_bytes, int round, void* stream);
 /* gd_query_async that also records `traversal_done` (a cudaEvent_t, may be

@@ -35,6 +35,8 @@ void query_traverse(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const Gd
                     void* ws, size_t ws_bytes, int round, int budget, cudaStream_t s);
 void query_finish(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg,
                   void* ws, size_t ws_bytes, GdResult* result_dev, cudaStream_t s);
+void query_round(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, const GdConfig& cfg, void* ws,
+                 size_t ws_bytes, GdResult* result_dev, cudaStream_t s, int round);
 void query_group_async(const GdMesh& ma, const GdMesh& mb, const GdBvh& a, const GdBvh& b, int n,
                        const GdConfig* cfgs, void* const* wss, const size_t* ws_bytes, void* const* host_dst,
                        int max_stats, cudaStream_t s, cudaEvent_t traversal_done, bool external_record);
@@ -202,9 +204,11 @@ int gd_query(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, const G
     GD_CHECK(mesh_a && mesh_b && a && b && cfg && out, GD_ERR_INVALID, "null argument");
     query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), nullptr);
     query_collect(*cfg, workspace, nullptr, out, stats, max_stats, S(stream));
-    // a front larger than the arena: one more round per leaf chunk
-    for (int r = 1; out->pending && out->status == 0; ++r) {
-      query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), nullptr, r);
+    // a front larger than the arena: one more round per leaf chunk; a band
+    // overflow: the rescan pass (query_round decides)
+    while (out->pending && out->status == 0) {
+      query_round(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream),
+                  out->rounds > 0 ? out->rounds : 1);
       query_collect(*cfg, workspace, nullptr, out, stats, max_stats, S(stream));
     }
     if (out->status == GD_ERR_WORKSPACE)
@@ -230,7 +234,7 @@ int gd_query_round(const GdMesh* mesh_a, const GdMesh* mesh_b, const GdBvh* a, c
   return guarded([&] {
     GD_CHECK(mesh_a && mesh_b && a && b && cfg, GD_ERR_INVALID, "null argument");
     GD_CHECK(round >= 1, GD_ERR_INVALID, "gd_query_round resumes a query: round must be >= 1");
-    query_async(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), nullptr, round);
+    query_round(*mesh_a, *mesh_b, *a, *b, *cfg, workspace, workspace_bytes, nullptr, S(stream), round);
   });
 }
 

@@ -81,6 +81,7 @@ struct alignas(16) QState {
   long long ov_cand, ov_in, ov_cap;
   float slack;
   int band_overflow;
+  int rescanned;                     // the rescan pass covered this round's band overflow (query_round)
   unsigned fbest;                    // best float32 narrow distance (ordered bits)
   unsigned dfs_coord;                // per-triangle DFS: max |coordinate| of A (float bits)
   unsigned long long visited;        // per-triangle DFS: node examinations

@@ -93,6 +93,7 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   const unsigned long long n = S->n_leaf;
   if (n == 0) return;
   if (kRescan && *reinterpret_cast<volatile int*>(&S->band_overflow) == 0) return;
+  if (kRescan && blockIdx.x == 0 && threadIdx.x == 0) S->rescanned = 1;  // read by the k_refine after it
   // this round's leaf-pair list and the candidate list (the arena's gap)
   const uint2* leaves = q.fnode + S->leaf_off;
   const float* keys = q.fkey + S->leaf_off;
@@ -352,7 +353,10 @@ constexpr int kRefineThreads = 64;
 template <bool kMax, int kOrder>
 // min: the lean float64 feature loop keeps ~150 registers live (no spills at
 // 4 blocks / SM: 41 -> 36 us on the rings); max is short and stays at 12
-__global__ __launch_bounds__(kRefineThreads, kMax ? 12 : 4) void k_refine(QArgs q) {
+#ifndef GD_REFINE_MINB
+#define GD_REFINE_MINB 4
+#endif
+__global__ __launch_bounds__(kRefineThreads, kMax ? 12 : GD_REFINE_MINB) void k_refine(QArgs q) {
   grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
   const unsigned long long n = min(S->n_band, q.band_cap);
@@ -512,7 +516,13 @@ __device__ void finalize(const QArgs& q) {
   r.overflow_front_in = S->ov_in;
   r.overflow_cap = S->ov_cap;
   r.rounds = S->rounds;
-  r.pending = S->pending;
+  // bit 0: levels remain (another traversal round); bit 1: the band or the
+  // candidate list overflowed and no rescan has covered it yet -- the record
+  // is not final, query_round runs the rescan pass and this exact pass again
+  r.pending = S->pending |
+              (*reinterpret_cast<volatile int*>(&S->band_overflow) && !*reinterpret_cast<volatile int*>(&S->rescanned)
+                   ? 2
+                   : 0);
   if (!found) {
     r.tri_a = r.tri_b = -1;
     const float b = load_bound(S);

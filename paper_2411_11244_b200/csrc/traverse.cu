@@ -95,6 +95,7 @@ __device__ void init_query(const QArgs& q) {
   S->culled = 0;
   S->band_eval = 0;
   S->band_overflow = 0;
+  S->rescanned = 0;
   S->ov_cand = S->ov_in = S->ov_cap = 0;
   if (q.A.depth == 0 && q.B.depth == 0) {
     q.fnode[0] = make_uint2(0, 0);
@@ -168,6 +169,7 @@ __device__ void resume_round(const QArgs& q) {
   S->n_band = 0;
   S->n_cand = 0;
   S->band_overflow = 0;
+  S->rescanned = 0;
   S->done = 0;
 }
 

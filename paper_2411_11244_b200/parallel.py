@@ -279,6 +279,21 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
     qs.wait_event(done)
     plans = [PreparedQuery(cur[0], cur[1], bvh_a, bvh_b, cfg, kind, private_workspace=True, frame=frame)
              for _ in range(2)]
+    def take(f, pq):
+        r = pq.fetch(rounds_ok=False)
+        if r is None:
+            # a chunked traversal (front larger than the arena): its later
+            # rounds would read boxes the next frame's refit may have
+            # rewritten -- wait for everything in flight, then this frame on
+            # its own (and the boxes back to the frame in flight after it)
+            torch.cuda.synchronize()
+            a, b = moved(f)
+            refit_frame(a, b)
+            r = PreparedQuery(a, b, bvh_a, bvh_b, cfg, kind, frame=frame).run()
+            refit_frame(*cur)
+            torch.cuda.synchronize()
+        local[f] = row(r)
+
     pending = None
     for i, f in enumerate(mine):
         if i:
@@ -293,9 +308,9 @@ def run_sequence(mesh_a, mesh_b, bvh_a, bvh_b, transforms, kind: str = "min", cf
             done = refit_on_rs(*nxt, after=trav)
             cur = nxt
         if pending is not None:
-            local[pending[0]] = row(pending[1].fetch())
+            take(*pending)
         pending = (f, pq)
-    local[pending[0]] = row(pending[1].fetch())
+    take(*pending)
     qs.wait_stream(rs)
     return gather_frames(len(transforms), local, group)
 

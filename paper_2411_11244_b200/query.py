@@ -420,12 +420,18 @@ class PreparedQuery:
         self._finish_rounds(self.res, s)
         return _result(self.kind, self.res, self.stats)
 
-    def _finish_rounds(self, res, s):
+    def _finish_rounds(self, res, s, rounds_ok: bool = True) -> bool:
         """A front larger than the arena is expanded in chunks: every leaf
-        chunk ends a traversal round, and the record says `pending` until the
-        last one (gd_query_round)."""
+        chunk ends a traversal round, and the record says `pending` (bit 0)
+        until the last one; a round whose band overflowed says bit 1 until the
+        rescan pass has run (gd_query_round decides; DESIGN.md "Front
+        arena", "Exactness").  rounds_ok=False: stop (return False) before a
+        further traversal round -- the caller's trees may already describe
+        another frame (pipelined sequences); the rescan pass reads no boxes."""
         L = _lib.lib()
         while res.pending and res.status == 0:
+            if not rounds_ok and not res.pending & 2:
+                return False
             _lib.check(L.gd_query_round(C.byref(self.g_ma), C.byref(self.g_mb), C.byref(self.g_a), C.byref(self.g_b),
                                         C.byref(self.g_cfg), _lib.ptr(self.ws), self.ws.numel(), int(res.rounds), s),
                        "query_round")
@@ -433,6 +439,7 @@ class PreparedQuery:
                                           _lib.ptr(self.ws), None, C.byref(self.res), self.stats, _MAX_STATS, s),
                        "query")
             res = self.res
+        return True
 
     def run(self) -> QueryResult:
         self.launch()
@@ -471,13 +478,16 @@ class PreparedQuery:
         self._ready.record()
         return self
 
-    def fetch(self) -> QueryResult:
+    def fetch(self, rounds_ok: bool = True) -> QueryResult | None:
+        """Wait for the launched query's record.  rounds_ok=False: None when
+        the query still needs traversal rounds (see _finish_rounds)."""
         self._ready.synchronize()
         base = self._pinned.data_ptr()
         r = _lib.GdResult.from_address(base)
         stats = (_lib.GdIterStat * _MAX_STATS).from_address(base + C.sizeof(_lib.GdResult))
         if r.pending and r.status == 0:
-            self._finish_rounds(r, _lib.stream_ptr())
+            if not self._finish_rounds(r, _lib.stream_ptr(), rounds_ok):
+                return None
             return _result(self.kind, self.res, self.stats)
         return _result(self.kind, r, stats)
 
@@ -596,14 +606,13 @@ class FrameGraph:
             base = buf.data_ptr()
             r = _lib.GdResult.from_address(base)
             stats = (_lib.GdIterStat * _MAX_STATS).from_address(base + C.sizeof(_lib.GdResult))
-            if r.pending and r.status == 0:  # a chunked traversal: the remaining rounds, synchronously
-                if self.overlapped:
-                    # the next frame's refits may already have rewritten the
-                    # boxes the remaining rounds would read: the caller
-                    # recomputes this frame (run_sequence_minmax)
+            if r.pending and r.status == 0:  # not final: the rescan pass / remaining rounds, synchronously
+                # (overlapped: the next frame's refits may already have
+                # rewritten the boxes further rounds would read -- then the
+                # caller recomputes this frame, run_sequence_minmax)
+                if not p._finish_rounds(r, _lib.stream_ptr(), rounds_ok=not self.overlapped):
                     out[kind] = None
                     continue
-                p._finish_rounds(r, _lib.stream_ptr())
                 out[kind] = _result(kind, p.res, p.stats)
             else:
                 out[kind] = _result(kind, r, stats)

@@ -112,6 +112,38 @@ def test_band_overflow_rescan(md, gpu):
         assert r.distance == base.distance
         assert (r.witness.tri_a, r.witness.tri_b) == (base.witness.tri_a, base.witness.tri_b)
         assert r.witness.point_a.tolist() == base.witness.point_a.tolist()
+        # the rescan pass is not in the launch sequence: the record says
+        # pending bit 1 until gd_query_round has run it (fetch, collect and the
+        # synchronous C loop all resume it)
+        pq.launch_fetch()
+        r = pq.fetch()
+        assert r.distance == base.distance and (r.witness.tri_a, r.witness.tri_b) == (base.witness.tri_a,
+                                                                                      base.witness.tri_b)
+        # band overflow in every round of a chunked traversal (pending bits 0
+        # and 1 together)
+        pq = Q.PreparedQuery(a, b, ta, tb, md.EngineConfig(arena_entries=1 << 10), kind)
+        pq.g_cfg.band_cap = 2
+        r = pq.run()
+        assert r.rounds > 1 and r.distance == base.distance, kind
+        assert (r.witness.tri_a, r.witness.tri_b) == (base.witness.tri_a, base.witness.tri_b)
+
+
+def test_pipelined_sequence_chunked_frames(md, gpu):
+    """run_sequence pipelines frame f + 1's refit against frame f's narrow
+    phases; a chunked frame (arena far too small) cannot resume its later
+    rounds after that refit, so it is recomputed on its own -- every frame
+    equals the plain API's answer."""
+    a0, b0 = md.ring_pair_base(120, 60)
+    ta, tb = md.build_f12(a0), md.build_f12(b0)
+    xfs = [md.ring_frame_transforms(f) for f in range(0, 56, 7)]
+    cfg = md.EngineConfig(front_hard_cap=1 << 30, arena_entries=1 << 10)
+    want = []
+    for xa, xb in xfs:
+        a, b = md.apply_transform(a0, xa), md.apply_transform(b0, xb)
+        want.append(md.run_min_query(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30)))
+    out = md.run_sequence(a0, b0, ta, tb, xfs, "min", cfg)
+    for f, w in enumerate(want):
+        assert out[f][0] == w.distance and (int(out[f][1]), int(out[f][2])) == (w.witness.tri_a, w.witness.tri_b), f
 
 
 @pytest.fixture(scope="module")
