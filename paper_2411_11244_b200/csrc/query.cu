@@ -224,6 +224,9 @@ static void launch_traverse(QArgs q, cudaStream_t s) {
 // k_nfilter<rescan>, k_refine.  pdl_first: the first kernel may overlap the
 // drain of the stream's previous kernel (its traversal); off when the chain
 // starts a side stream after an event wait.
+#ifndef GD_NTEST_BLOCKS
+#define GD_NTEST_BLOCKS 2  // k_ntest blocks per SM = its resident capacity at 105 registers: one wave striding over the list (4: 0.3469 ms, 2: 0.3464 ms rings min; nested shells min 26.46 -> 26.18 ms)
+#endif
 template <bool kMax>
 static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
   const int sms = num_sms();
@@ -234,7 +237,7 @@ static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
   // when the phases are not being timed
   if (g_profile) {
     k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
-    if (!kMax) k_ntest<kMax><<<sms * 4, 256, 0, s>>>(q);
+    if (!kMax) k_ntest<kMax><<<sms * GD_NTEST_BLOCKS, 256, 0, s>>>(q);
     mark(3);
     launch_refine<kMax>(q, s, false);  // + witness record in its last block
   } else {
@@ -242,7 +245,7 @@ static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
       launch_pdl(k_nfilter<kMax, false>, sms * 8, 256, s, q);
     else
       k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
-    if (!kMax) launch_pdl(k_ntest<kMax>, sms * 4, 256, s, q);
+    if (!kMax) launch_pdl(k_ntest<kMax>, sms * GD_NTEST_BLOCKS, 256, s, q);
     launch_refine<kMax>(q, s, true);
   }
   mark(4);
