@@ -86,6 +86,20 @@ __device__ __forceinline__ bool axis_separated(const Tri<float>& a, const Tri<fl
 //    triangles, than a candidate round trip.
 //  * kRescan (only after a band / candidate overflow): every survivor of the
 //    final bound is evaluated in the reference arithmetic right here.
+// grid: GD_NFILTER_BLOCKS (min) / GD_NFILTER_BLOCKS_MAX (max) blocks per SM,
+// striding over the leaf pairs.  k_nfilter<max> (92 registers, 2 resident
+// blocks / SM) runs a short list in its first resident wave only -- the rings'
+// max query 0.214 -> 0.199 ms -- and a long one (near-contact scenes) over
+// the whole grid, whose later blocks balance the uneven per-pair work
+// (nested shells max 304 ms vs 334 ms with 3 blocks / SM throughout).
+#ifndef GD_NFILTER_BLOCKS
+#define GD_NFILTER_BLOCKS 8
+#endif
+#ifndef GD_NFILTER_BLOCKS_MAX
+#define GD_NFILTER_BLOCKS_MAX 6
+#endif
+constexpr int kNfilterMaxWave = 2;                 // blocks per SM of the short-list wave
+constexpr unsigned long long kNfilterShortList = 1ull << 21;  // leaf pairs
 template <bool kMax, bool kRescan>
 __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   grid_dependency_wait();  // programmatic dependent launch (query.cu)
@@ -109,7 +123,10 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   rbest.hi = ~0ull;
   rbest.lo = ~0ull;
   const float fb_rescan = kRescan ? __uint_as_float(*reinterpret_cast<volatile unsigned*>(&S->fbest)) : 0.f;
-  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned blocks = gridDim.x;
+  if (kMax && !kRescan && n <= kNfilterShortList) blocks = max(1u, gridDim.x * kNfilterMaxWave / GD_NFILTER_BLOCKS_MAX);
+  if (blockIdx.x >= blocks) return;
+  const unsigned long long stride = (unsigned long long)blocks * blockDim.x;
   for (unsigned long long base = (unsigned long long)blockIdx.x * blockDim.x; base < n; base += stride) {
     const unsigned long long i = base + threadIdx.x;
     const float ub = load_bound(S), ub2 = ub * ub;

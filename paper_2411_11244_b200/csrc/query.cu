@@ -236,15 +236,15 @@ static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
   // profiling events between the kernels would serialise them: PDL only
   // when the phases are not being timed
   if (g_profile) {
-    k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
+    k_nfilter<kMax, false><<<sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS), 256, 0, s>>>(q);
     if (!kMax) k_ntest<kMax><<<sms * GD_NTEST_BLOCKS, 256, 0, s>>>(q);
     mark(3);
     launch_refine<kMax>(q, s, false);  // + witness record in its last block
   } else {
     if (pdl_first)
-      launch_pdl(k_nfilter<kMax, false>, sms * 8, 256, s, q);
+      launch_pdl(k_nfilter<kMax, false>, sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS), 256, s, q);
     else
-      k_nfilter<kMax, false><<<sms * 8, 256, 0, s>>>(q);
+      k_nfilter<kMax, false><<<sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS), 256, 0, s>>>(q);
     if (!kMax) launch_pdl(k_ntest<kMax>, sms * GD_NTEST_BLOCKS, 256, s, q);
     launch_refine<kMax>(q, s, true);
   }
