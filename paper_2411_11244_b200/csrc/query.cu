@@ -151,6 +151,9 @@ static unsigned refine_grid() {
   if (g[dev] == 0) {
     int per_sm = 0;
     GD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine<kMax, kOrder>, kRefineThreads, 0));
+#ifdef GD_REFINE_PER_SM
+    per_sm = std::min(per_sm, GD_REFINE_PER_SM);
+#endif
     g[dev] = (unsigned)(std::max(per_sm, 1) * num_sms());
   }
   return g[dev];
