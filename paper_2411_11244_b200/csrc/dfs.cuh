@@ -54,6 +54,8 @@ __global__ void k_dfs_init(QArgs q) {
   S->narrow = 0;
   S->band_eval = 0;
   S->band_overflow = 0;
+  S->rescanned = 0;
+  S->n_cand = 0;  // no candidate list: k_refine reads the band only (direct_exact with 0 candidates)
   S->ov_cand = S->ov_in = S->ov_cap = 0;
   S->visited = 0;
 }

@@ -270,6 +270,24 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
   }
 }
 
+// Short candidate lists (min queries) skip the float32 stage: k_refine
+// evaluates every candidate in the reference arithmetic right away.  The
+// band's float32 window exists to spare exact evaluations when the list is
+// long (near-contact scenes: 70M candidates, 38M in the band); on a short
+// list the exact pass is one latency-bound wave either way, and the float32
+// test before it cost ~35 us on the rings (39K candidates, 29K of them in the
+// band).  Exact either way: the candidates are a superset of the band, every
+// key is an achieved exact distance, and the optimum pairs are among them.
+#ifndef GD_DIRECT_EXACT
+#define GD_DIRECT_EXACT (1ull << 16)
+#endif
+constexpr unsigned long long kDirectExact = GD_DIRECT_EXACT;
+__device__ __forceinline__ bool direct_exact(const QState* S) {
+  const volatile QState* V = S;
+  const unsigned long long n = V->n_cand;
+  return n <= kDirectExact && n <= V->cand_cap;  // (a longer list overflowed: the rescan covers it)
+}
+
 // Narrow phase, stage 2 (k_ntest, min queries): the float32 triangle-pair
 // test on the dense candidate list; updates the bound and fills the band.
 template <bool kMax>
@@ -277,7 +295,7 @@ __global__ __launch_bounds__(256) void k_ntest(QArgs q) {
   grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
   const unsigned long long n = min(S->n_cand, S->cand_cap);
-  if (n == 0) return;
+  if (n == 0 || (!kMax && direct_exact(S))) return;  // a short list: k_refine evaluates it exactly
   if (blockIdx.x * 256ull >= n) return;
   const uint2* cand = q.fnode + S->cand_off;
   const float E = S->slack;
@@ -377,6 +395,12 @@ __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : GD_REFINE_MINB) void k_
   grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
   const unsigned long long n = min(S->n_band, q.band_cap);
+  // a short candidate list (min): every candidate after the band entries
+  // (then only a warm pair), evaluated exactly (direct_exact)
+  const bool direct = !kMax && direct_exact(S);
+  const unsigned long long n_all = n + (direct ? S->n_cand : 0ull);
+  const uint2* cand = q.fnode + S->cand_off;
+  if (direct && blockIdx.x == 0 && threadIdx.x == 0 && S->n_cand) atomicAdd(&S->narrow, S->n_cand);
   const float E = S->slack;
   const float fb = __uint_as_float(*reinterpret_cast<volatile unsigned*>(&S->fbest));
   __shared__ Key128 wk[kRefineThreads / 32];
@@ -386,11 +410,22 @@ __global__ __launch_bounds__(kRefineThreads, kMax ? 12 : GD_REFINE_MINB) void k_
   best.hi = ~0ull;
   best.lo = ~0ull;
   unsigned long long evals = 0;
-  for (unsigned long long j = (unsigned long long)blockIdx.x * kRefineThreads + threadIdx.x; j < n;
+  for (unsigned long long j = (unsigned long long)blockIdx.x * kRefineThreads + threadIdx.x; j < n_all;
        j += (unsigned long long)gridDim.x * kRefineThreads) {
-    const float f = q.band_d[j];
-    const uint2 ids = q.band_ids[j];  // loaded with f: no second dependent round trip
-    if (!(kMax ? f >= fb - E : f <= fb + E)) continue;  // +-inf (warm pair) always passes
+    uint2 ids;
+    if (j < n) {
+      const float f = q.band_d[j];
+      ids = q.band_ids[j];  // loaded with f: no second dependent round trip
+      if (!(kMax ? f >= fb - E : f <= fb + E)) continue;  // +-inf (warm pair) always passes
+    } else {
+      // candidate (leaf rank * 2 + triangle) pair -> triangle ids (the 5th
+      // word of the leaves' leaf_tri records, as k_ntest reads them)
+      const uint2 c = cand[j - n];
+      const float4 fa = __ldg(reinterpret_cast<const float4*>(q.A.leaf_tri) + 5 * (unsigned long long)(c.x >> 1) + 4);
+      const float4 fb4 = __ldg(reinterpret_cast<const float4*>(q.B.leaf_tri) + 5 * (unsigned long long)(c.y >> 1) + 4);
+      ids = make_uint2((unsigned)__float_as_int((c.x & 1) ? fa.w : fa.z),
+                       (unsigned)__float_as_int((c.y & 1) ? fb4.w : fb4.z));
+    }
     const Key128 k = exact_key<kMax, kOrder>(q, ids.x, ids.y);
     if (key_less(k, best)) best = k;
     ++evals;

@@ -548,3 +548,21 @@ def test_query_group_matches_separate(md, gpu, scene):
     with pytest.raises(ValueError, match="share"):
         other = md.PreparedQuery(b, a, tb, ta, cfg, "min", private_workspace=True)
         md.launch_group([plans["min"], other])
+
+
+@pytest.mark.parametrize("lat_lon, long_list", [((16, 20), False), ((130, 160), True)])
+def test_narrow_paths_short_and_long_lists(md, gpu, lat_lon, long_list):
+    """Min queries evaluate a short candidate list (<= 2^16 triangle pairs)
+    exactly right away and a long one through the float32 band
+    (narrow.cuh direct_exact); nested shells are near contact everywhere, so
+    both sizes are reached -- both equal the device brute force (distance and
+    lexicographic witness), in float64 and float32."""
+    lat, lon = lat_lon
+    a, b = md.gen_scene("nested-shells", {"lat": lat, "lon": lon, "r_inner": 0.8, "r_outer": 0.81})
+    for prec in (64, 32):
+        dt = np.float64 if prec == 64 else np.float32
+        ta, tb = md.build_f12(a, dtype=dt), md.build_f12(b, dtype=dt)
+        r = md.run_min_query(a, b, ta, tb, md.EngineConfig(precision=prec, front_hard_cap=1 << 30))
+        assert (r.narrow_pairs > 1 << 16) == long_list, r.narrow_pairs
+        d, w = md.brute_force_min(a, b, force=True, dtype=dt)
+        assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (w.tri_a, w.tri_b), prec
