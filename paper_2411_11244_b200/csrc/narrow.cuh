@@ -279,7 +279,7 @@ __global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
 // band).  Exact either way: the candidates are a superset of the band, every
 // key is an achieved exact distance, and the optimum pairs are among them.
 #ifndef GD_DIRECT_EXACT
-#define GD_DIRECT_EXACT (1ull << 16)
+#define GD_DIRECT_EXACT (1ull << 18)
 #endif
 constexpr unsigned long long kDirectExact = GD_DIRECT_EXACT;
 __device__ __forceinline__ bool direct_exact(const QState* S) {

@@ -550,9 +550,9 @@ def test_query_group_matches_separate(md, gpu, scene):
         md.launch_group([plans["min"], other])
 
 
-@pytest.mark.parametrize("lat_lon, long_list", [((16, 20), False), ((130, 160), True)])
+@pytest.mark.parametrize("lat_lon, long_list", [((16, 20), False), ((260, 300), True)])
 def test_narrow_paths_short_and_long_lists(md, gpu, lat_lon, long_list):
-    """Min queries evaluate a short candidate list (<= 2^16 triangle pairs)
+    """Min queries evaluate a short candidate list (<= 2^18 triangle pairs)
     exactly right away and a long one through the float32 band
     (narrow.cuh direct_exact); nested shells are near contact everywhere, so
     both sizes are reached -- both equal the device brute force (distance and
@@ -563,6 +563,6 @@ def test_narrow_paths_short_and_long_lists(md, gpu, lat_lon, long_list):
         dt = np.float64 if prec == 64 else np.float32
         ta, tb = md.build_f12(a, dtype=dt), md.build_f12(b, dtype=dt)
         r = md.run_min_query(a, b, ta, tb, md.EngineConfig(precision=prec, front_hard_cap=1 << 30))
-        assert (r.narrow_pairs > 1 << 16) == long_list, r.narrow_pairs
+        assert (r.narrow_pairs > 1 << 18) == long_list, r.narrow_pairs
         d, w = md.brute_force_min(a, b, force=True, dtype=dt)
         assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (w.tri_a, w.tri_b), prec
