@@ -566,3 +566,21 @@ def test_narrow_paths_short_and_long_lists(md, gpu, lat_lon, long_list):
         assert (r.narrow_pairs > 1 << 18) == long_list, r.narrow_pairs
         d, w = md.brute_force_min(a, b, force=True, dtype=dt)
         assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (w.tri_a, w.tri_b), prec
+
+
+def test_min_rescan_after_band_overflow_long_list(md, gpu):
+    """A long candidate list (> 2^18, the float32 stage runs) with a 2-entry
+    band: the band overflows, the record says pending bit 1, and the rescan
+    pass (host-driven through gd_query_round) still returns the brute-force
+    answer."""
+    from paper_2411_11244_b200 import query as Q
+
+    a, b = md.gen_scene("nested-shells", {"lat": 260, "lon": 300, "r_inner": 0.8, "r_outer": 0.81})
+    ta, tb = md.build_f12(a), md.build_f12(b)
+    pq = Q.PreparedQuery(a, b, ta, tb, md.EngineConfig(front_hard_cap=1 << 30), "min")
+    pq.g_cfg.band_cap = 2
+    pq.launch()
+    r = pq.collect()  # collect sees pending bit 1 and runs the rescan itself
+    assert r.narrow_pairs > 1 << 18
+    d, w = md.brute_force_min(a, b, force=True)
+    assert r.distance == d and (r.witness.tri_a, r.witness.tri_b) == (w.tri_a, w.tri_b)
