@@ -154,6 +154,9 @@ static unsigned refine_grid() {
 #ifdef GD_REFINE_PER_SM
     per_sm = std::min(per_sm, GD_REFINE_PER_SM);
 #endif
+    // max: the band's exact test is 9 vertex pairs -- 4 blocks / SM instead of
+    // the resident 12 (fewer arrivals on the done counter): rings max 0.1988 -> 0.1966 ms
+    if (kMax) per_sm = std::min(per_sm, 4);
     g[dev] = (unsigned)(std::max(per_sm, 1) * num_sms());
   }
   return g[dev];
