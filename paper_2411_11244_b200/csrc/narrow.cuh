@@ -100,8 +100,12 @@ __device__ __forceinline__ bool axis_separated(const Tri<float>& a, const Tri<fl
 #endif
 constexpr int kNfilterMaxWave = 2;                 // blocks per SM of the short-list wave
 constexpr unsigned long long kNfilterShortList = 1ull << 21;  // leaf pairs
+#ifndef GD_NFILTER_THREADS
+#define GD_NFILTER_THREADS 256
+#endif
+constexpr int kNfilterThreads = GD_NFILTER_THREADS;
 template <bool kMax, bool kRescan>
-__global__ __launch_bounds__(256) void k_nfilter(QArgs q) {
+__global__ __launch_bounds__(kNfilterThreads) void k_nfilter(QArgs q) {
   grid_dependency_wait();  // programmatic dependent launch (query.cu)
   QState* S = q.S;
   const unsigned long long n = S->n_leaf;

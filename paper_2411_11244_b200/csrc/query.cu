@@ -242,15 +242,15 @@ static void launch_narrow(const QArgs& q, cudaStream_t s, bool pdl_first) {
   // profiling events between the kernels would serialise them: PDL only
   // when the phases are not being timed
   if (g_profile) {
-    k_nfilter<kMax, false><<<sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS), 256, 0, s>>>(q);
+    k_nfilter<kMax, false><<<sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS) * (256 / kNfilterThreads), kNfilterThreads, 0, s>>>(q);
     if (!kMax) k_ntest<kMax><<<sms * GD_NTEST_BLOCKS, 256, 0, s>>>(q);
     mark(3);
     launch_refine<kMax>(q, s, false);  // + witness record in its last block
   } else {
     if (pdl_first)
-      launch_pdl(k_nfilter<kMax, false>, sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS), 256, s, q);
+      launch_pdl(k_nfilter<kMax, false>, sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS) * (256 / kNfilterThreads), kNfilterThreads, s, q);
     else
-      k_nfilter<kMax, false><<<sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS), 256, 0, s>>>(q);
+      k_nfilter<kMax, false><<<sms * (kMax ? GD_NFILTER_BLOCKS_MAX : GD_NFILTER_BLOCKS) * (256 / kNfilterThreads), kNfilterThreads, 0, s>>>(q);
     if (!kMax) launch_pdl(k_ntest<kMax>, sms * GD_NTEST_BLOCKS, 256, s, q);
     launch_refine<kMax>(q, s, true);
   }
@@ -357,7 +357,7 @@ template <bool kMax>
 static void launch_rescan(const QArgs& q, cudaStream_t s) {
   const int sms = num_sms();
   GD_CUDA(cudaMemsetAsync(&q.S->done, 0, sizeof(unsigned), s));
-  k_nfilter<kMax, true><<<sms * 4, 256, 0, s>>>(q);
+  k_nfilter<kMax, true><<<sms * 4 * (256 / kNfilterThreads), kNfilterThreads, 0, s>>>(q);
   launch_refine<kMax>(q, s, false);
   GD_CUDA(cudaGetLastError());
   count_launches(2);
