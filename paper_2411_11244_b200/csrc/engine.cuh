@@ -97,6 +97,7 @@ struct alignas(16) QState {
   unsigned long long t_it[kMaxIters + 1];      // %globaltimer at iteration boundaries
   unsigned long long t_sweep[kMaxIters];       // last block's sweep end (profiling)
   unsigned long long t_plan[kMaxIters + 1];    // block 0: next sweep planned after iteration i's barrier
+  unsigned long long t_edge[3];                // profiling: k_traverse entry, prologue barrier passed, exit (block 0)
 };
 
 

@@ -119,6 +119,13 @@ int phase_ms(float* out, int n) {
     // then the planning after each barrier (commit + plan of the next sweep, block 0)
     for (int i = 0; i < iters && k < n; ++i, ++k)
       out[k] = (float)((double)(pl[i + 1] > t[i + 1] ? pl[i + 1] - t[i + 1] : 0) * 1e-6);
+    // then k_traverse's edges (block 0): entry -> prologue barrier passed,
+    // barrier -> first sweep planned, last sweep -> exit
+    unsigned long long e[3];
+    GD_CUDA(cudaMemcpy(e, g_last_state->t_edge, sizeof(e), cudaMemcpyDeviceToHost));
+    if (k < n) out[k++] = (float)((double)(e[1] - e[0]) * 1e-6);
+    if (k < n) out[k++] = (float)((double)(t[0] > e[1] ? t[0] - e[1] : 0) * 1e-6);
+    if (k < n) out[k++] = (float)((double)(e[2] > t[iters] ? e[2] - t[iters] : 0) * 1e-6);
   }
   return k;
 }

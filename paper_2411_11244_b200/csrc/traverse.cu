@@ -887,6 +887,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
   if (cont && !V->paused) return;
   if (threadIdx.x == 0) qs = q;
   const bool rec = blockIdx.x == 0 && threadIdx.x == 0;
+  if (rec && q.profile) S->t_edge[0] = globaltimer_ns();
   if (blockIdx.x == 0) {
     if (q.round == 0) {
       if (threadIdx.x == 0) init_query<kMax>(q);
@@ -905,6 +906,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
     if (threadIdx.x < 3) S->cnt[threadIdx.x] = 0;
   }
   prologue_barrier(&S->epoch_flag, q.epoch);
+  if (rec && q.profile) S->t_edge[1] = globaltimer_ns();
   for (int i = threadIdx.x; i < kMaxIters; i += blockDim.x) {
     t.tot_cand[i] = V->tot_cand[i];
     t.tot_in[i] = V->tot_in[i];
@@ -998,6 +1000,7 @@ __device__ __forceinline__ void traverse_round(const QArgs& q) {
       for (int i = 0; i < t.iter; ++i) skipped += V->skip_it[i];
     S->ncand_total = t.ncand_total;
     S->expanded = t.ncand_total - skipped;  // candidates of the pairs this call owns
+    if (q.profile) S->t_edge[2] = globaltimer_ns();
   }
 }
 

@@ -52,6 +52,10 @@ for warm in (None, "self"):
     out = {"warm": warm, "distance": r.distance, "witness": [r.witness.tri_a, r.witness.tri_b],
            "phases_ms": dict(zip(["init", "expand", "narrow", "exact", "final"], [round(x, 4) for x in ph[:5]])),
            "expanded": r.expanded_pairs, "narrow_pairs": r.narrow_pairs, "band": r.band_pairs,
+           "edges_ms": {"prologue": round(ph[5 + 3 * len(r.iterations)], 4),
+                        "first_plan": round(ph[6 + 3 * len(r.iterations)], 4),
+                        "epilogue": round(ph[7 + 3 * len(r.iterations)], 4)}
+           if 7 + 3 * len(r.iterations) < len(ph) else None,
            "iters": [{"k": s.k, "in": s.front_in, "out": s.front_out, "culled": s.culled,
                       "bound": round(s.bound_after, 6), "ms": round(ph[5 + i], 4) if 5 + i < len(ph) else None,
                       "sweep_ms": round(ph[5 + len(r.iterations) + i], 4)
